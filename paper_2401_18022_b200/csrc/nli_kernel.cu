@@ -1,0 +1,444 @@
+// ISRS-GN numerical-integral NLI kernels for sm_100a (FP64).
+//
+// Reference algorithm: nli_psd_at / kernel_abs2 (gn_integral.hpp:136-313).
+// The hyperbolic-coordinate Riemann sum is generated from indices on the
+// device; nothing about the (u1, u2) grid is materialised in HBM.
+//
+// Work decomposition:
+//   unit  = one u1-row (probe, quadrant q, row i); a persistent grid of warps
+//           pulls rows from an atomic queue.
+//   warp  = one row.  Lanes first evaluate the per-point setup for 32 u2
+//           columns at a time (coordinates, 3x psd_at, 3 stencils, phi,
+//           gn_integral.hpp:288-303), then the two 16-lane half-warps each take
+//           one evaluated point and split its distance steps across lanes
+//           (step m = lane + 16 k), so the table loads are coalesced, the
+//           fast/slow branch (gn_integral.hpp:156) is uniform per half-warp,
+//           and every lane does exp2 + sincos per step.
+//   reduce= fixed-order xor-shuffle tree per point, points summed into the row
+//           in ascending j (reference order), rows Kahan-summed in ascending i
+//           by the finalize kernel (gn_integral.hpp:258,306) -> deterministic,
+//           independent of grid size, CTA scheduling and GPU partitioning.
+//
+// Fast branch uses summation by parts of the reference's phasor-difference
+// sum:  sum_m p_m (E_{m+1} - E_m) = -p_0 E_0 + sum_{e>=1} (p_{e-1} - p_e) E_e
+// (p_N = 0), so each step needs ONE sincos (at its end edge) and one shuffle.
+//
+// This file is compiled with -fmad=false: all setup arithmetic rounds exactly
+// like the reference (no contraction); the hot loop uses explicit fma().
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+
+#include "nli_kernel.cuh"
+#include "uwb_devmath.cuh"
+
+namespace uwb {
+
+namespace {
+
+constexpr int kWarps = 8;  // warps per CTA
+constexpr unsigned kFull = 0xffffffffu;
+
+__constant__ double c_exp2_tab[32] = UWB_EXP2_TABLE;
+
+// ChannelGrid::psd_at (channel_grid.hpp:35-42) fused with stencil_for
+// (gn_integral.hpp:110-129): both start from the same `pos`.
+struct Stencil {
+  int i0, i1;
+  double hw0, hw1;
+};
+
+__device__ __forceinline__ double psd_and_stencil(const NliParams& P, double nu, Stencil* s) {
+  const double pos = (nu - P.freq[0]) / P.spacing;
+  double psd = 0.0;
+  const long i = lround(pos);
+  if (i >= 0 && i < P.n_ch) {
+    if (!(fabs(nu - __ldg(P.freq + i)) > 0.5 * P.bch)) psd = __ldg(P.psd + i);
+  }
+  s->i0 = 0;
+  s->i1 = 0;
+  s->hw0 = 0.5;
+  s->hw1 = 0.0;
+  const int n = P.n_ch;
+  if (n == 1 || pos <= 0.0) return psd;
+  if (pos >= static_cast<double>(n - 1)) {
+    s->i0 = s->i1 = n - 1;
+    return psd;
+  }
+  const int k = static_cast<int>(pos);  // pos in (0, n-1): truncation == size_t cast
+  const double t = pos - static_cast<double>(k);
+  s->i0 = k;
+  s->i1 = k + 1;
+  s->hw0 = 0.5 * (1.0 - t);
+  s->hw1 = 0.5 * t;
+  return psd;
+}
+
+// phase_mismatch (gn_integral.hpp:43-50), same grouping; -fmad=false keeps
+// every product/sum separately rounded like the reference.
+__device__ __forceinline__ double phase_mismatch(double f1, double f2, double fi, double b2,
+                                                 double b3, double b4) {
+  const double quartic =
+      (f1 * f1 + f2 * f2) + 1.5 * (f1 * f2) + 3.0 * fi * (f1 + f2) + 3.0 * (fi * fi);
+  const double bracket = b2 + kPi * b3 * ((f1 + f2) + 2.0 * fi) +
+                         (2.0 * kPi * kPi / 3.0) * b4 * quartic;
+  return -4.0 * kPi * kPi * (f1 * f2) * bracket;
+}
+
+// Per-warp shared state for one chunk of 32 u2 columns.
+struct WarpSmem {
+  int col[6][32];    // stencil columns i0/i1 for nu1, nu2, nu3
+  double w[6][32];   // matching half weights
+  double phi[32];
+  double pw[32];     // p1 * p2 * p3
+  int src[32];       // chunk-local column of the listed point
+  double val[32];    // pw * |kernel|^2 per chunk column
+};
+
+// |sum over spans & steps|^2 for one point, computed by one 16-lane segment.
+template <int K>
+__device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSmem& S, int idx,
+                                               int probe, int sl, unsigned segmask,
+                                               const double* tab) {
+  const int N = P.steps;
+  const double phi = S.phi[idx];
+  const double w0 = S.w[0][idx], w1 = S.w[1][idx], w2 = S.w[2][idx];
+  const double w3 = S.w[3][idx], w4 = S.w[4][idx], w5 = S.w[5][idx];
+  const size_t o0 = static_cast<size_t>(S.col[0][idx]) * N;
+  const size_t o1 = static_cast<size_t>(S.col[1][idx]) * N;
+  const size_t o2 = static_cast<size_t>(S.col[2][idx]) * N;
+  const size_t o3 = static_cast<size_t>(S.col[3][idx]) * N;
+  const size_t o4 = static_cast<size_t>(S.col[4][idx]) * N;
+  const size_t o5 = static_cast<size_t>(S.col[5][idx]) * N;
+  double fre = 0.0, fim = 0.0, sre = 0.0, sim = 0.0;
+  for (int k = 0; k < P.n_spans; ++k) {
+    const double* T = P.log2rho + k * P.span_stride;
+    const double* hl = P.hl2 + (static_cast<size_t>(probe) * P.n_spans + k) * N;
+    double p[K];
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) {
+      const int m = sl + 16 * kk;
+      p[kk] = 0.0;
+      if (m < N) {
+        double lg = fma(w0, __ldg(T + o0 + m), -__ldg(hl + m));
+        lg = fma(w1, __ldg(T + o1 + m), lg);
+        lg = fma(w2, __ldg(T + o2 + m), lg);
+        lg = fma(w3, __ldg(T + o3 + m), lg);
+        lg = fma(w4, __ldg(T + o4 + m), lg);
+        lg = fma(w5, __ldg(T + o5 + m), lg);
+        p[kk] = exp2_pos(lg, tab);
+      }
+    }
+    const bool fast = fabs(phi) * __ldg(P.wlast + k) > 1e-4;
+    if (fast) {
+      const double* ze = P.zedge + static_cast<size_t>(k) * (N + 1);
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        const int m = sl + 16 * kk;
+        // p_{m+1}: next lane, or lane 0 of the next step block for lane 15.
+        double pn = __shfl_down_sync(segmask, p[kk], 1, 16);
+        const double pw = (kk + 1 < K) ? __shfl_sync(segmask, p[kk + 1 < K ? kk + 1 : kk], 0, 16)
+                                       : 0.0;
+        if (sl == 15) pn = pw;
+        if (m < N) {
+          const double c = p[kk] - pn;
+          double cs, sn;
+          sincos_rd(phi * __ldg(ze + m + 1), &cs, &sn);
+          fre = fma(c, cs, fre);
+          fim = fma(c, sn, fim);
+        }
+      }
+      if (sl == 0) {
+        const double z0 = __ldg(ze);
+        double c0 = 1.0, s0 = 0.0;
+        if (z0 != 0.0) sincos_rd(phi * z0, &c0, &s0);
+        fre = fma(-p[0], c0, fre);
+        fim = fma(-p[0], s0, fim);
+      }
+    } else {
+      const double* zm = P.zmid + static_cast<size_t>(k) * N;
+      const double* wd = P.width + static_cast<size_t>(k) * N;
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        const int m = sl + 16 * kk;
+        if (m < N) {
+          const double wm = __ldg(wd + m);
+          // sinc(x), |x| = |phi| w/2 <= 5e-5 on this branch: 1 - x^2/6 + x^4/120 is exact
+          const double x = 0.5 * phi * wm;
+          const double x2 = x * x;
+          const double sinc = fma(x2, fma(x2, 1.0 / 120.0, -1.0 / 6.0), 1.0);
+          const double w = p[kk] * wm * sinc;
+          double cs, sn;
+          sincos_rd(phi * __ldg(zm + m), &cs, &sn);
+          sre = fma(w, cs, sre);
+          sim = fma(w, sn, sim);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 8; o >= 1; o >>= 1) {
+    fre += __shfl_xor_sync(segmask, fre, o, 16);
+    fim += __shfl_xor_sync(segmask, fim, o, 16);
+    sre += __shfl_xor_sync(segmask, sre, o, 16);
+    sim += __shfl_xor_sync(segmask, sim, o, 16);
+  }
+  // fast spans contribute (sum / (j phi)) (gn_integral.hpp:173-175)
+  const double re = sre + fim / phi;
+  const double im = sim - fre / phi;
+  return re * re + im * im;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParams P) {
+  __shared__ double s_tab[32];
+  __shared__ WarpSmem s_w[kWarps];
+  if (threadIdx.x < 32) s_tab[threadIdx.x] = c_exp2_tab[threadIdx.x];
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int sl = lane & 15;
+  const int seg = lane >> 4;
+  const unsigned segmask = 0xffffu << (16 * seg);
+  WarpSmem& S = s_w[warp];
+  const int per_probe = P.n_q * P.n_r;
+
+  for (;;) {
+    int row = 0;
+    if (lane == 0) row = static_cast<int>(atomicAdd(P.counter, 1u));
+    row = __shfl_sync(kFull, row, 0);
+    if (row >= P.total_rows) break;
+    const int probe = row / per_probe;
+    const int rem = row - probe * per_probe;
+    const int q = rem / P.n_r + 1;
+    const int i = rem - (q - 1) * P.n_r;
+    const double nu = __ldg(P.probe_nu + probe);
+    const double f = nu - P.centre;
+
+    // quadrant_limits (gn_integral.hpp:63-79)
+    const double bm = P.half_band - f, bp = P.half_band + f;
+    double b1, b2, s1, s2;
+    switch (q) {
+      case 1: b1 = bm; b2 = bm; s1 = 1.0; s2 = 1.0; break;
+      case 2: b1 = bp; b2 = bm; s1 = -1.0; s2 = 1.0; break;
+      case 3: b1 = bp; b2 = bp; s1 = -1.0; s2 = -1.0; break;
+      default: b1 = bm; b2 = bp; s1 = 1.0; s2 = -1.0; break;
+    }
+    const double u1_max = b1 * b2;
+    if (!(u1_max > 0.0)) {
+      if (lane == 0) P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
+      continue;
+    }
+    // u1 bin (gn_integral.hpp:262-286)
+    const int n_r = P.n_r;
+    double e0, e1;
+    if (P.u1_uniform) {
+      e0 = u1_max * static_cast<double>(i) / n_r;
+      e1 = u1_max * static_cast<double>(i + 1) / n_r;
+    } else {
+      e0 = i == 0 ? 0.0 : u1_max * exp(P.ln_min * static_cast<double>(n_r - i) / (n_r - 1));
+      e1 = u1_max * exp(P.ln_min * static_cast<double>(n_r - i - 1) / (n_r - 1));
+    }
+    const double du1 = e1 - e0;
+    const double u1 = (e0 == 0.0 || P.u1_uniform) ? 0.5 * (e0 + e1) : sqrt(e0 * e1);
+    const double su = sqrt(u1);
+    const double hi = log(b1 / su);
+    const double lo = -log(b2 / su);
+    if (!(hi > lo)) {
+      if (lane == 0) P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
+      continue;
+    }
+    const double du2 = (hi - lo) / n_r;
+    double row_acc = 0.0;
+    unsigned n_eval = 0;
+
+    for (int jb = 0; jb < n_r; jb += 32) {
+      // ---- per-point setup, one u2 column per lane (gn_integral.hpp:288-303)
+      const int j = jb + lane;
+      bool active = false;
+      bool fast = false;
+      Stencil st1, st2, st3;
+      double phi = 0.0, pw = 0.0;
+      if (j < n_r) {
+        const double u2 = lo + (static_cast<double>(j) + 0.5) * du2;
+        const double g1 = su * exp(u2);
+        const double g2 = u1 / g1;
+        const double f1 = s1 * g1;
+        const double f2 = s2 * g2;
+        const double p1 = psd_and_stencil(P, nu + f1, &st1);
+        const double p2 = psd_and_stencil(P, nu + f2, &st2);
+        const double p3 = psd_and_stencil(P, nu + f1 + f2, &st3);
+        active = p1 != 0.0 && p2 != 0.0 && p3 != 0.0;
+        if (active) {
+          phi = phase_mismatch(f1, f2, f, P.beta2, P.beta3, P.beta4);
+          pw = p1 * p2 * p3;
+          fast = fabs(phi) * __ldg(P.wlast) > 1e-4;
+        }
+      }
+      const unsigned am = __ballot_sync(kFull, active);
+      const unsigned fm = __ballot_sync(kFull, active && fast);
+      const unsigned sm = am & ~fm;
+      const unsigned lt = (1u << lane) - 1u;
+      S.val[lane] = 0.0;
+      if (active) {
+        // fast points first, then slow ones, so half-warp pairs rarely diverge
+        const int pos = fast ? __popc(fm & lt) : __popc(fm) + __popc(sm & lt);
+        S.col[0][pos] = st1.i0; S.col[1][pos] = st1.i1;
+        S.col[2][pos] = st2.i0; S.col[3][pos] = st2.i1;
+        S.col[4][pos] = st3.i0; S.col[5][pos] = st3.i1;
+        S.w[0][pos] = st1.hw0; S.w[1][pos] = st1.hw1;
+        S.w[2][pos] = st2.hw0; S.w[3][pos] = st2.hw1;
+        S.w[4][pos] = st3.hw0; S.w[5][pos] = st3.hw1;
+        S.phi[pos] = phi;
+        S.pw[pos] = pw;
+        S.src[pos] = lane;
+      }
+      __syncwarp();
+      const int n_act = __popc(am);
+      n_eval += n_act;
+      for (int idx = seg; idx < n_act; idx += 2) {
+        const double kv = point_kernel<K>(P, S, idx, probe, sl, segmask, s_tab);
+        if (sl == 0) S.val[S.src[idx]] = S.pw[idx] * kv;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int lim = min(32, n_r - jb);
+        for (int t = 0; t < lim; ++t) row_acc += S.val[t];  // ascending j
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      P.rowsum[row] = row_acc * du1 * du2;
+      atomicAdd(P.n_eval, static_cast<unsigned long long>(n_eval));
+    }
+  }
+}
+
+// Probe half-log columns (gn_integral.hpp:234-251), in log2 units, plus the
+// per-probe quadrant_limits validity check done on the host.
+__global__ void probe_halflog_kernel(const NliParams P) {
+  const int probe = blockIdx.x;
+  const double nu = P.probe_nu[probe];
+  Stencil sc;
+  psd_and_stencil(P, nu, &sc);
+  for (int k = 0; k < P.n_spans; ++k) {
+    const double* T = P.log2rho + k * P.span_stride;
+    double* out = P.hl2 + (static_cast<size_t>(probe) * P.n_spans + k) * P.steps;
+    for (int m = threadIdx.x; m < P.steps; m += blockDim.x) {
+      out[m] = sc.hw0 * T[static_cast<size_t>(sc.i0) * P.steps + m] +
+               sc.hw1 * T[static_cast<size_t>(sc.i1) * P.steps + m];
+    }
+  }
+}
+
+// Kahan sum over rows in ascending i per quadrant (gn_integral.hpp:258,306),
+// Q4 mirror (:310) and G = 16/27 gamma^2 sum_q (:312).
+__global__ void finalize_probes_kernel(const NliParams P, const FinalizeParams F) {
+  const int probe = blockIdx.x * blockDim.x + threadIdx.x;
+  if (probe >= F.n_probes) return;
+  double quad[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int q = 0; q < P.n_q; ++q) {
+    const double* rs = P.rowsum + (static_cast<size_t>(probe) * P.n_q + q) * P.n_r;
+    double sum = 0.0, comp = 0.0;
+    for (int i = 0; i < P.n_r; ++i) {
+      const double x = rs[i];
+      if (isnan(x)) continue;
+      const double y = x - comp;
+      const double t = sum + y;
+      comp = (t - sum) - y;
+      sum = t;
+    }
+    quad[q] = sum;
+  }
+  if (F.mirror_q4) quad[3] = quad[1];
+  const double g = F.probe_gamma[probe];
+  F.probe_g[probe] = (16.0 / 27.0) * g * g * (quad[0] + quad[1] + quad[2] + quad[3]);
+  for (int q = 0; q < 4; ++q) F.probe_quad[4 * probe + q] = quad[q];
+}
+
+// channel_nli + the all_channels_nli epilogue (gn_integral.hpp:316-359).
+__global__ void finalize_channels_kernel(const FinalizeParams F) {
+  const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ch >= F.n_ch) return;
+  const int p0 = F.chan_probe0[ch];
+  if (p0 < 0) {
+    F.eta[ch] = F.nli_psd[ch] = F.nli_power[ch] = 0.0;
+    for (int q = 0; q < 4; ++q) F.quad[4 * ch + q] = 0.0;
+    F.skipped[ch] = 1;
+    return;
+  }
+  double psd = F.probe_g[p0];
+  if (F.simpson) psd = (F.probe_g[p0 + 1] + 4.0 * psd + F.probe_g[p0 + 2]) / 6.0;
+  const double p = F.psd[ch] * F.bch;
+  F.nli_psd[ch] = psd;
+  F.nli_power[ch] = psd * F.bch;
+  F.eta[ch] = F.nli_power[ch] / (p * p * p);
+  for (int q = 0; q < 4; ++q) F.quad[4 * ch + q] = F.probe_quad[4 * p0 + q];
+  F.skipped[ch] = 0;
+}
+
+using RowKernel = void (*)(const NliParams);
+
+RowKernel row_kernel_for(int steps) {
+  switch ((steps + 15) / 16) {
+    case 1: return nli_rows_kernel<1>;
+    case 2: return nli_rows_kernel<2>;
+    case 3: return nli_rows_kernel<3>;
+    case 4: return nli_rows_kernel<4>;
+    case 5: return nli_rows_kernel<5>;
+    case 6: return nli_rows_kernel<6>;
+    case 7: return nli_rows_kernel<7>;
+    case 8: return nli_rows_kernel<8>;
+    case 9: return nli_rows_kernel<9>;
+    case 10: return nli_rows_kernel<10>;
+    case 11: return nli_rows_kernel<11>;
+    case 12: return nli_rows_kernel<12>;
+    case 13: return nli_rows_kernel<13>;
+    case 14: return nli_rows_kernel<14>;
+    case 15: return nli_rows_kernel<15>;
+    case 16: return nli_rows_kernel<16>;
+    default: return nullptr;
+  }
+}
+
+}  // namespace
+
+int launch_finalize_channels_only(const FinalizeParams& f, cudaStream_t st) {
+  finalize_channels_kernel<<<(f.n_ch + 127) / 128, 128, 0, st>>>(f);
+  return 1;
+}
+
+int nli_ctas_per_sm(int steps) {
+  RowKernel k = row_kernel_for(steps);
+  if (!k) return 0;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kWarps * 32, 0) != cudaSuccess) return 0;
+  return n;
+}
+
+int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaStream_t stream,
+               cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
+  RowKernel k = row_kernel_for(p.steps);
+  if (!k || p.n_probes <= 0) return -1;
+  int launches = 0;
+  cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), stream);
+  cudaMemsetAsync(p.n_eval, 0, sizeof(unsigned long long), stream);
+  probe_halflog_kernel<<<p.n_probes, 128, 0, stream>>>(p);
+  ++launches;
+  if (ev_k0) cudaEventRecord(ev_k0, stream);
+  k<<<grid_ctas, kWarps * 32, 0, stream>>>(p);
+  ++launches;
+  if (ev_k1) cudaEventRecord(ev_k1, stream);
+  finalize_probes_kernel<<<(f.n_probes + 127) / 128, 128, 0, stream>>>(p, f);
+  ++launches;
+  if (f.n_ch > 0) {
+    finalize_channels_kernel<<<(f.n_ch + 127) / 128, 128, 0, stream>>>(f);
+    ++launches;
+  }
+  return launches;
+}
+
+}  // namespace uwb

@@ -1,0 +1,76 @@
+// Device-side data layout and launch interface of the ISRS-GN NLI engine.
+// See DESIGN.md §3 for the HBM layout and the roofline of each kernel.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace uwb {
+
+// Everything the integrand kernel reads.  All pointers are device memory.
+struct NliParams {
+  // ChannelGrid (channel_grid.hpp:15-22)
+  int n_ch;
+  const double* freq;
+  const double* psd;
+  double spacing, bch, centre, half_band;
+  // Spans: log2(rho) tables [span][ch][m] (reference layout ch*steps+m, scaled
+  // by log2 e so the integrand can use exp2), span-absolute edge/mid, widths.
+  int n_spans;
+  int steps;
+  const double* log2rho;  // [n_spans * n_ch * steps] (span k at k * span_stride)
+  size_t span_stride;     // n_ch * steps, or 0 when every span shares one table
+  const double* zedge;    // [n_spans * (steps + 1)] = z_base + edge
+  const double* zmid;     // [n_spans * steps]       = z_base + mid
+  const double* width;    // [n_spans * steps]
+  const double* wlast;    // [n_spans] width.back(): fast/slow switch (gn_integral.hpp:156)
+  double beta2, beta3, beta4;
+  // GnSolverConfig
+  int n_r;
+  int u1_uniform;
+  double ln_min;  // log(u1_min_ratio), host-computed
+  int n_q;        // 3 with mirror_q4, else 4
+  // probes
+  int n_probes;
+  const double* probe_nu;  // [n_probes]
+  double* hl2;             // [n_probes * n_spans * steps] log2 half-power of the probe
+  // work queue + outputs
+  int total_rows;               // n_probes * n_q * n_r
+  unsigned int* counter;        // row queue head (zeroed before launch)
+  unsigned long long* n_eval;   // evaluated-point counter (stats)
+  double* rowsum;               // [total_rows]; NaN => row not added (reference `continue`)
+};
+
+struct FinalizeParams {
+  // per probe
+  int n_probes;
+  const double* probe_gamma;  // [n_probes]
+  double* probe_g;            // [n_probes] (16/27) gamma^2 sum_q quad
+  double* probe_quad;         // [n_probes * 4]
+  int mirror_q4;
+  // per channel (n_ch = 0 skips the channel stage: nli_psd_at mode)
+  int n_ch;
+  const double* psd;       // launch PSD per channel
+  double bch;
+  int simpson;
+  const int* chan_probe0;  // [n_ch] first probe of the channel or -1 (skipped)
+  double* eta;
+  double* nli_psd;
+  double* nli_power;
+  double* quad;      // [n_ch * 4]
+  uint8_t* skipped;  // [n_ch]
+};
+
+// Issue the NLI pipeline on `stream`: queue reset, probe half-log columns,
+// integrand rows (persistent, grid_ctas CTAs), per-probe and per-channel
+// finalize.  ev_k0/ev_k1 (may be null) bracket the integrand kernel.
+// Returns the number of kernel launches (memset excluded).
+int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaStream_t stream,
+               cudaEvent_t ev_k0, cudaEvent_t ev_k1);
+
+// CTAs per SM the integrand kernel reaches for a given step count.
+int nli_ctas_per_sm(int steps);
+constexpr int kMaxSteps = 256;  // 16 lanes x 16 steps per lane
+
+}  // namespace uwb

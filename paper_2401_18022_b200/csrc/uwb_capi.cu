@@ -1,0 +1,432 @@
+// C-ABI of the ISRS-GN NLI engine (include/uwb_nli.h): validation with the
+// reference's error contract, HBM upload of the path's inputs, probe
+// construction, launch and read-back.  Host side only; kernels live in
+// nli_kernel.cu / raman_ode.cu / link_report.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/uwb_nli.h"
+#include "nli_kernel.cuh"
+#include "uwb_capi_internal.cuh"
+#include "uwb_ctx.cuh"
+#include "uwb_devmath.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+}  // namespace
+
+namespace uwb {
+
+int fail(int code, const std::string& msg) { return set_err(code, msg); }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return set_err(UWB_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Validate the grid as ChannelGrid::validate does (channel_grid.hpp:44-61).
+int validate_grid(const uwb_grid* g) {
+  if (!g || g->n_ch < 1 || !g->freq || !g->psd || !g->guard)
+    return fail(UWB_CONFIG_ERROR, "channel grid is empty");
+  if (!(g->spacing > 0.0) || !(g->bch > 0.0))
+    return fail(UWB_CONFIG_ERROR, "grid spacing and width must be > 0");
+  if (g->bch > g->spacing + 1e-9) return fail(UWB_CONFIG_ERROR, "channel width exceeds spacing");
+  for (int i = 0; i < g->n_ch; ++i) {
+    if (g->psd[i] < 0.0) return fail(UWB_CONFIG_ERROR, "negative launch PSD");
+    if (i > 0 && !(g->freq[i] > g->freq[i - 1]))
+      return fail(UWB_CONFIG_ERROR, "grid must ascend in frequency");
+  }
+  return UWB_OK;
+}
+
+// Upload the grid + span tables; fills the grid/span part of NliParams.
+int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_span* spans,
+                       const double beta[3], NliParams* P) {
+  // nli_psd_at's checks, in the reference's order (gn_integral.hpp:223-240)
+  if (n_spans <= 0 || !spans) return fail(UWB_CONFIG_ERROR, "nli_psd_at: need at least one span");
+  const int n = g->n_ch;
+  const int steps = spans[0].steps;
+  for (int k = 0; k < n_spans; ++k) {
+    if (spans[k].steps != steps)
+      return fail(UWB_CONFIG_ERROR, "uwb: all spans must share one distance-step count");
+    if (!spans[k].log_rho || !spans[k].edge || !spans[k].mid || !spans[k].width)
+      return fail(UWB_CONFIG_ERROR, "nli_psd_at: span evolution does not match the channel grid");
+  }
+  if (steps < 1 || steps > kMaxSteps)
+    return fail(UWB_CONFIG_ERROR, "uwb: distance steps per span must be in [1, 256]");
+
+  std::vector<double> tab(static_cast<size_t>(n_spans) * n * steps);
+  std::vector<double> ze(static_cast<size_t>(n_spans) * (steps + 1));
+  std::vector<double> zm(static_cast<size_t>(n_spans) * steps);
+  std::vector<double> wd(static_cast<size_t>(n_spans) * steps);
+  std::vector<double> wl(n_spans);
+  double z_base = 0.0;
+  for (int k = 0; k < n_spans; ++k) {
+    const uwb_span& s = spans[k];
+    double* t = tab.data() + static_cast<size_t>(k) * n * steps;
+    for (size_t x = 0; x < static_cast<size_t>(n) * steps; ++x) t[x] = s.log_rho[x] * kLog2e;
+    for (int m = 0; m <= steps; ++m) ze[static_cast<size_t>(k) * (steps + 1) + m] = z_base + s.edge[m];
+    for (int m = 0; m < steps; ++m) {
+      zm[static_cast<size_t>(k) * steps + m] = z_base + s.mid[m];
+      wd[static_cast<size_t>(k) * steps + m] = s.width[m];
+    }
+    wl[k] = s.width[steps - 1];
+    z_base += s.length;
+  }
+  double* d_freq = c->freq.get<double>(n);
+  double* d_psd = c->psd.get<double>(n);
+  double* d_tab = c->log2rho.get<double>(tab.size());
+  double* d_ze = c->zedge.get<double>(ze.size());
+  double* d_zm = c->zmid.get<double>(zm.size());
+  double* d_wd = c->width.get<double>(wd.size());
+  double* d_wl = c->wlast.get<double>(wl.size());
+  if (!d_freq || !d_psd || !d_tab || !d_ze || !d_zm || !d_wd || !d_wl)
+    return fail(UWB_CUDA_ERROR, "device allocation failed");
+  cudaStream_t st = c->stream;
+  cudaMemcpyAsync(d_freq, g->freq, n * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_psd, g->psd, n * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_ze, ze.data(), ze.size() * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_zm, zm.data(), zm.size() * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_wd, wd.data(), wd.size() * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_wl, wl.data(), wl.size() * sizeof(double), cudaMemcpyHostToDevice, st);
+  // the vectors die at return: make the copies complete first
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "upload");
+
+  P->n_ch = n;
+  P->freq = d_freq;
+  P->psd = d_psd;
+  P->spacing = g->spacing;
+  P->bch = g->bch;
+  P->centre = g->centre;
+  P->half_band = g->half_band;
+  P->n_spans = n_spans;
+  P->steps = steps;
+  P->log2rho = d_tab;
+  P->span_stride = static_cast<size_t>(n) * steps;
+  P->zedge = d_ze;
+  P->zmid = d_zm;
+  P->width = d_wd;
+  P->wlast = d_wl;
+  P->beta2 = beta[0];
+  P->beta3 = beta[1];
+  P->beta4 = beta[2];
+  return UWB_OK;
+}
+
+int set_cfg(const uwb_nli_cfg* cfg, NliParams* P) {
+  if (!cfg) return fail(UWB_CONFIG_ERROR, "missing solver config");
+  if (cfg->n_r < 2) return fail(UWB_CONFIG_ERROR, "nli_psd_at: n_r must be >= 2");
+  P->n_r = cfg->n_r;
+  P->u1_uniform = cfg->u1_uniform ? 1 : 0;
+  P->ln_min = std::log(cfg->u1_min_ratio);
+  P->n_q = cfg->mirror_q4 ? 3 : 4;
+  return UWB_OK;
+}
+
+// Upload probes, run the pipeline, leave results in the context buffers.
+int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vector<double>& nu,
+               const std::vector<double>& gam, const std::vector<int>* chan_probe0,
+               bool sync_stats) {
+  // quadrant_limits' range check (gn_integral.hpp:64-66), probe by probe
+  for (double v : nu) {
+    const double f = v - P.centre;
+    if (std::abs(f) > P.half_band)
+      return fail(UWB_CONFIG_ERROR,
+                  "quadrant_limits: channel offset must lie inside the half band");
+  }
+  const int np = static_cast<int>(nu.size());
+  FinalizeParams F{};
+  F.n_probes = np;
+  F.mirror_q4 = cfg->mirror_q4 ? 1 : 0;
+  c->last_launches = 0;
+  c->last_kernel_ms = 0.0;
+  c->last_inner_steps = 0.0;
+  c->last_points = 0.0;
+  if (np == 0 && !chan_probe0) return UWB_OK;
+  double* d_nu = c->probe_nu.get<double>(std::max(np, 1));
+  double* d_g = c->probe_gamma.get<double>(std::max(np, 1));
+  P.n_probes = np;
+  P.total_rows = np * P.n_q * P.n_r;
+  P.probe_nu = d_nu;
+  P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * P.steps);
+  P.rowsum = c->rowsum.get<double>(std::max(P.total_rows, 1));
+  P.counter = c->counter.get<unsigned int>(1);
+  P.n_eval = c->n_eval.get<unsigned long long>(1);
+  F.probe_gamma = d_g;
+  F.probe_g = c->probe_g.get<double>(std::max(np, 1));
+  F.probe_quad = c->probe_quad.get<double>(4 * std::max(np, 1));
+  if (!P.hl2 || !P.rowsum || !P.counter || !F.probe_g || !F.probe_quad || !d_nu || !d_g)
+    return fail(UWB_CUDA_ERROR, "device allocation failed");
+  cudaStream_t st = c->stream;
+  if (np) {
+    cudaMemcpyAsync(d_nu, nu.data(), np * sizeof(double), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_g, gam.data(), np * sizeof(double), cudaMemcpyHostToDevice, st);
+  }
+  if (chan_probe0) {
+    const int n = P.n_ch;
+    int* d_cp = c->chan_probe0.get<int>(n);
+    F.n_ch = n;
+    F.psd = P.psd;
+    F.bch = P.bch;
+    F.simpson = cfg->simpson ? 1 : 0;
+    F.chan_probe0 = d_cp;
+    F.eta = c->eta.get<double>(n);
+    F.nli_psd = c->nli_psd.get<double>(n);
+    F.nli_power = c->nli_power.get<double>(n);
+    F.quad = c->quad.get<double>(4 * n);
+    F.skipped = c->skipped.get<uint8_t>(n);
+    cudaMemcpyAsync(d_cp, chan_probe0->data(), n * sizeof(int), cudaMemcpyHostToDevice, st);
+  }
+  cudaEventRecord(c->ev0, st);
+  if (np) {
+    const int per_sm = nli_ctas_per_sm(P.steps);
+    if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
+    const int launched = launch_nli(P, F, c->sm_count * per_sm, st, c->evk0, c->evk1);
+    if (launched < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
+    c->last_launches = launched;
+  } else {
+    // every channel skipped: only the channel epilogue
+    c->last_launches = launch_finalize_channels_only(F, st);
+  }
+  cudaEventRecord(c->ev1, st);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "launch");
+  if (sync_stats) {
+    e = cudaEventSynchronize(c->ev1);
+    if (e != cudaSuccess) return cuda_fail(e, "nli kernels");
+    float ms = 0.f;
+    if (np) {
+      cudaEventElapsedTime(&ms, c->evk0, c->evk1);
+      c->last_kernel_ms = ms;
+      unsigned long long ne = 0;
+      cudaMemcpy(&ne, P.n_eval, sizeof ne, cudaMemcpyDeviceToHost);
+      c->last_points = static_cast<double>(ne);
+      c->last_inner_steps = static_cast<double>(ne) * P.steps * P.n_spans;
+    }
+  }
+  return UWB_OK;
+}
+
+// Probe list of all_channels_nli (gn_integral.hpp:348-353, channel_nli :316-329).
+void channel_probes(const uwb_grid* g, const double* gamma, const uwb_nli_cfg* cfg,
+                    const std::vector<int>& subset, std::vector<double>* nu,
+                    std::vector<double>* gam, std::vector<int>* chan_probe0) {
+  const int n = g->n_ch;
+  std::vector<uint8_t> want(n, subset.empty() ? 1 : 0);
+  for (int ch : subset)
+    if (ch >= 0 && ch < n) want[ch] = 1;
+  chan_probe0->assign(n, -1);
+  for (int ch = 0; ch < n; ++ch) {
+    if (!want[ch] || g->guard[ch] || g->psd[ch] <= 0.0) continue;
+    (*chan_probe0)[ch] = static_cast<int>(nu->size());
+    const double f = g->freq[ch];
+    nu->push_back(f);
+    gam->push_back(gamma[ch]);
+    if (cfg->simpson) {
+      nu->push_back(f - 0.5 * g->bch);
+      gam->push_back(gamma[ch]);
+      nu->push_back(f + 0.5 * g->bch);
+      gam->push_back(gamma[ch]);
+    }
+  }
+}
+
+}  // namespace uwb
+
+using namespace uwb;
+
+extern "C" {
+
+const char* uwb_last_error(void) { return g_err.c_str(); }
+
+int uwb_abi_version(void) { return UWB_ABI_VERSION; }
+
+int uwb_ctx_create(int device, uwb_ctx** out) {
+  if (!out) return set_err(UWB_CONFIG_ERROR, "null output");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return set_err(UWB_CUDA_ERROR, "no CUDA device visible (the engine has no CPU fallback)");
+  if (device < 0 || device >= n) return set_err(UWB_CONFIG_ERROR, "device index out of range");
+  cudaDeviceProp prop;
+  if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return cuda_fail(e, "props");
+  if (prop.major < 10)
+    return set_err(UWB_CUDA_ERROR, "the engine is built for sm_100a (B200); device is sm_" +
+                                       std::to_string(prop.major) + std::to_string(prop.minor));
+  if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  auto* c = new uwb_ctx();
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  c->cc_major = prop.major;
+  c->cc_minor = prop.minor;
+  if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "stream");
+  }
+  cudaEventCreate(&c->ev0);
+  cudaEventCreate(&c->ev1);
+  cudaEventCreate(&c->evk0);
+  cudaEventCreate(&c->evk1);
+  // probe the kernel image: fails loudly if the fatbin has no sm_100a code
+  if (nli_ctas_per_sm(112) <= 0) {
+    uwb_ctx_destroy(c);
+    return set_err(UWB_CUDA_ERROR, "integrand kernel not loadable on this device");
+  }
+  *out = c;
+  return UWB_OK;
+}
+
+void uwb_ctx_destroy(uwb_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  release_link_state(c);
+  for (DBuf* b : {&c->freq, &c->psd, &c->gamma, &c->log2rho, &c->zedge, &c->zmid, &c->width,
+                  &c->wlast, &c->probe_nu, &c->probe_gamma, &c->hl2, &c->rowsum, &c->counter,
+                  &c->n_eval, &c->probe_g, &c->probe_quad, &c->chan_probe0, &c->eta, &c->nli_psd,
+                  &c->nli_power, &c->quad, &c->skipped, &c->alpha, &c->aeff, &c->raman_x,
+                  &c->raman_y, &c->nf_db, &c->guard, &c->rho_end, &c->ode_work, &c->report,
+                  &c->mid, &c->edge})
+    b->release();
+  if (c->pinned) cudaFreeHost(c->pinned);
+  for (cudaEvent_t ev : {c->ev0, c->ev1, c->evk0, c->evk1})
+    if (ev) cudaEventDestroy(ev);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int uwb_device_info(uwb_ctx* c, int* sm_count, int* cc_major, int* cc_minor) {
+  if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  if (sm_count) *sm_count = c->sm_count;
+  if (cc_major) *cc_major = c->cc_major;
+  if (cc_minor) *cc_minor = c->cc_minor;
+  return UWB_OK;
+}
+
+int uwb_set_channel_subset(uwb_ctx* c, int n, const int* channels) {
+  if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  c->subset.assign(channels, channels + std::max(n, 0));
+  if (n > 0 && !channels) return set_err(UWB_CONFIG_ERROR, "null channel list");
+  return UWB_OK;
+}
+
+int uwb_all_channels_nli(uwb_ctx* c, const uwb_grid* grid, int n_spans, const uwb_span* spans,
+                         const double beta[3], const double* gamma, const uwb_nli_cfg* cfg,
+                         uwb_nli_result* out) {
+  if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  cudaSetDevice(c->device);
+  release_link_state(c);  // shares buffers with the prepared evaluation
+  int rc = validate_grid(grid);
+  if (rc) return rc;
+  NliParams P{};
+  if ((rc = set_cfg(cfg, &P))) return rc;
+  if (!gamma) return set_err(UWB_CONFIG_ERROR, "missing per-channel gamma");
+  std::vector<double> nu, gam;
+  std::vector<int> cp;
+  channel_probes(grid, gamma, cfg, c->subset, &nu, &gam, &cp);
+  // Like the reference, an all-guard grid never reaches nli_psd_at's checks.
+  if (!nu.empty()) {
+    if ((rc = upload_path_inputs(c, grid, n_spans, spans, beta, &P))) return rc;
+  } else {
+    const int n = grid->n_ch;
+    P.n_ch = n;
+    P.psd = c->psd.get<double>(n);
+    P.bch = grid->bch;
+    cudaMemcpyAsync(const_cast<double*>(P.psd), grid->psd, n * sizeof(double),
+                    cudaMemcpyHostToDevice, c->stream);
+  }
+  if ((rc = run_probes(c, P, cfg, nu, gam, &cp, true))) return rc;
+  const int n = grid->n_ch;
+  cudaStream_t st = c->stream;
+  if (out) {
+    if (out->eta) cudaMemcpyAsync(out->eta, c->eta.ptr<double>(), n * 8, cudaMemcpyDeviceToHost, st);
+    if (out->nli_psd)
+      cudaMemcpyAsync(out->nli_psd, c->nli_psd.ptr<double>(), n * 8, cudaMemcpyDeviceToHost, st);
+    if (out->nli_power)
+      cudaMemcpyAsync(out->nli_power, c->nli_power.ptr<double>(), n * 8, cudaMemcpyDeviceToHost, st);
+    if (out->quadrant)
+      cudaMemcpyAsync(out->quadrant, c->quad.ptr<double>(), n * 32, cudaMemcpyDeviceToHost, st);
+    if (out->skipped)
+      cudaMemcpyAsync(out->skipped, c->skipped.ptr<uint8_t>(), n, cudaMemcpyDeviceToHost, st);
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "all_channels_nli");
+  if (out) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    out->elapsed_seconds = ms * 1e-3;
+  }
+  return UWB_OK;
+}
+
+int uwb_nli_psd_at(uwb_ctx* c, const uwb_grid* grid, int n_spans, const uwb_span* spans,
+                   const double beta[3], const uwb_nli_cfg* cfg, int n_probe, const double* nu,
+                   const double* gamma, double* out, double* quadrant4) {
+  if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  cudaSetDevice(c->device);
+  release_link_state(c);
+  int rc = validate_grid(grid);
+  if (rc) return rc;
+  NliParams P{};
+  if ((rc = upload_path_inputs(c, grid, n_spans, spans, beta, &P))) return rc;
+  if ((rc = set_cfg(cfg, &P))) return rc;
+  if (n_probe <= 0) return UWB_OK;
+  std::vector<double> vnu(nu, nu + n_probe), vg(gamma, gamma + n_probe);
+  if ((rc = run_probes(c, P, cfg, vnu, vg, nullptr, true))) return rc;
+  cudaStream_t st = c->stream;
+  if (out) cudaMemcpyAsync(out, c->probe_g.ptr<double>(), n_probe * 8, cudaMemcpyDeviceToHost, st);
+  if (quadrant4)
+    cudaMemcpyAsync(quadrant4, c->probe_quad.ptr<double>(), n_probe * 32, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "nli_psd_at");
+  return UWB_OK;
+}
+
+int uwb_channel_nli(uwb_ctx* c, const uwb_grid* grid, int n_spans, const uwb_span* spans,
+                    const double beta[3], double gamma_ch, const uwb_nli_cfg* cfg, int ch,
+                    double* out, double* quadrant4) {
+  if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  if (!grid || ch < 0 || ch >= grid->n_ch) return set_err(UWB_CONFIG_ERROR, "channel out of range");
+  if (!cfg) return set_err(UWB_CONFIG_ERROR, "missing solver config");
+  const double f = grid->freq[ch];
+  double nu[3] = {f, f - 0.5 * grid->bch, f + 0.5 * grid->bch};
+  double g3[3] = {gamma_ch, gamma_ch, gamma_ch};
+  double res[3] = {0, 0, 0};
+  double q12[12];
+  const int np = cfg->simpson ? 3 : 1;
+  int rc = uwb_nli_psd_at(c, grid, n_spans, spans, beta, cfg, np, nu, g3, res, q12);
+  if (rc) return rc;
+  double psd_c = res[0];
+  if (cfg->simpson) psd_c = (res[1] + 4.0 * psd_c + res[2]) / 6.0;
+  if (out) *out = psd_c;
+  if (quadrant4) std::memcpy(quadrant4, q12, 4 * sizeof(double));
+  return UWB_OK;
+}
+
+int uwb_last_launch_count(uwb_ctx* c) { return c ? c->last_launches : 0; }
+
+int uwb_last_nli_stats(uwb_ctx* c, double* kernel_ms, double* inner_steps,
+                       double* evaluated_points) {
+  if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  if (kernel_ms) *kernel_ms = c->last_kernel_ms;
+  if (inner_steps) *inner_steps = c->last_inner_steps;
+  if (evaluated_points) *evaluated_points = c->last_points;
+  return UWB_OK;
+}
+
+}  // extern "C"

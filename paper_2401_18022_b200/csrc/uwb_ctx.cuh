@@ -1,0 +1,77 @@
+// Context object behind the C-ABI: device, stream, and the HBM-resident
+// buffers that persist across calls.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "nli_kernel.cuh"
+
+namespace uwb {
+
+// Grow-only device allocation.
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T>
+  T* get(size_t n) {
+    const size_t bytes = n * sizeof(T) + 16;
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+      cap = bytes;
+    }
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* ptr() const {
+    return static_cast<T*>(p);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+}  // namespace uwb
+
+struct uwb_ctx {
+  int device = 0;
+  int sm_count = 0;
+  int cc_major = 0, cc_minor = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;
+  // channel grid
+  uwb::DBuf freq, psd, gamma;
+  // spans
+  uwb::DBuf log2rho, zedge, zmid, width, wlast;
+  // probes + work
+  uwb::DBuf probe_nu, probe_gamma, hl2, rowsum, counter, n_eval, probe_g, probe_quad, chan_probe0;
+  // per-channel results
+  uwb::DBuf eta, nli_psd, nli_power, quad, skipped;
+  // link evaluation state (raman ODE + assembly)
+  uwb::DBuf alpha, aeff, raman_x, raman_y, nf_db, guard, rho_end, ode_work, report, mid, edge;
+  std::vector<int> subset;
+  // stats of the last call
+  int last_launches = 0;
+  double last_kernel_ms = 0.0;
+  double last_inner_steps = 0.0;
+  double last_points = 0.0;
+  // pinned host staging for small transfers
+  void* pinned = nullptr;
+  size_t pinned_cap = 0;
+  // prepared link problem (uwb_evaluate_link_prepare)
+  struct Prepared;
+  Prepared* prep = nullptr;
+};

@@ -1,0 +1,163 @@
+// FP64 transcendentals for the NLI integrand, written for the B200 FP64 pipe.
+//
+// The integrand's inner step (gn_integral.hpp:161-172) needs one exp and one
+// (cos, sin) pair per distance step.  CUDA's libdevice exp/sincos cost ~25 and
+// ~41 DFMA-equivalents on sm_100a (measured, profiles/r01_microbench.md): they
+// carry Payne-Hanek slow paths and overflow handling this path never needs.
+// These versions are branch-free, use only DFMA/DMUL/DADD plus integer ops on
+// the exponent, and stay within ~2 ulp of glibc:
+//   exp2_pos  : 2^x via k = rint(32x), 32-entry 2^(j/32) table, degree-6
+//               Taylor polynomial on |r| <= 1/64 (trunc. error 3.4e-18)
+//               -> 10 FP64 instructions.
+//   sincos_rd : Cody-Waite reduction by pi/2 with an exact FMA first part
+//               (valid |x| < 2^50), fdlibm minimax kernels on [-pi/4, pi/4]
+//               -> 19 FP64 instructions, quadrant fix-up on the ALU pipe.
+// Both are __host__ __device__ so tests/ can compare them with libm on CPU.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#if defined(__CUDACC__)
+#define UWB_HD __host__ __device__ __forceinline__
+#else
+#define UWB_HD inline
+#endif
+
+namespace uwb {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kLog2e = 1.4426950408889634074;
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: rint via addition
+
+UWB_HD int lo_word(double x) {
+#if defined(__CUDA_ARCH__)
+  return __double2loint(x);
+#else
+  uint64_t u;
+  std::memcpy(&u, &x, 8);
+  return static_cast<int>(static_cast<uint32_t>(u));
+#endif
+}
+
+UWB_HD int hi_word(double x) {
+#if defined(__CUDA_ARCH__)
+  return __double2hiint(x);
+#else
+  uint64_t u;
+  std::memcpy(&u, &x, 8);
+  return static_cast<int>(static_cast<uint32_t>(u >> 32));
+#endif
+}
+
+UWB_HD double from_words(int hi, int lo) {
+#if defined(__CUDA_ARCH__)
+  return __hiloint2double(hi, lo);
+#else
+  const uint64_t u = (static_cast<uint64_t>(static_cast<uint32_t>(hi)) << 32) |
+                     static_cast<uint32_t>(lo);
+  double x;
+  std::memcpy(&x, &u, 8);
+  return x;
+#endif
+}
+
+UWB_HD double fmad(double a, double b, double c) {
+#if defined(__CUDA_ARCH__)
+  return __fma_rn(a, b, c);
+#else
+  return std::fma(a, b, c);
+#endif
+}
+
+// 2^(j/32), j = 0..31, correctly rounded (generated with 60-digit arithmetic).
+#define UWB_EXP2_TABLE \
+  {1.0, 1.0218971486541166, 1.0442737824274138, 1.0671404006768237,  \
+   1.0905077326652577, 1.1143867425958924, 1.1387886347566916, 1.1637248587775775,  \
+   1.189207115002721, 1.215247359980469, 1.241857812073484, 1.2690509571917332,  \
+   1.2968395546510096, 1.3252366431597413, 1.3542555469368927, 1.383909881963832,  \
+   1.4142135623730951, 1.4451808069770467, 1.4768261459394993, 1.5091644275934228,  \
+   1.5422108254079407, 1.5759808451078865, 1.6104903319492543, 1.645755478153965,  \
+   1.681792830507429, 1.718619298122478, 1.7562521603732995, 1.7947090750031072,  \
+   1.8340080864093424, 1.8741676341103, 1.9152065613971474, 1.9571441241754002}
+
+// Taylor coefficients of 2^r = exp(r ln2): (ln 2)^n / n!
+constexpr double kE2c1 = 0.69314718055994530942;
+constexpr double kE2c2 = 0.24022650695910071233;
+constexpr double kE2c3 = 0.055504108664821579953;
+constexpr double kE2c4 = 0.0096181291076284771620;
+constexpr double kE2c5 = 0.0013333558146428443423;
+constexpr double kE2c6 = 0.00015403530393381609954;
+
+// 2^x for |x| < 1000 (the path's log2 power ratios are O(10)).  `tab` is the
+// 32-entry table above (shared memory on the device).
+UWB_HD double exp2_pos(double x, const double* tab) {
+  const double t = fmad(x, 32.0, kMagic);
+  const int k = lo_word(t);
+  const double kd = t - kMagic;
+  const double r = fmad(kd, -0.03125, x);  // exact: x - k/32, |r| <= 1/64
+  double p = fmad(kE2c6, r, kE2c5);
+  p = fmad(p, r, kE2c4);
+  p = fmad(p, r, kE2c3);
+  p = fmad(p, r, kE2c2);
+  p = fmad(p, r, kE2c1);
+  p = fmad(p, r, 1.0);
+  const double s = tab[k & 31] * p;
+  return from_words(hi_word(s) + ((k >> 5) << 20), lo_word(s));
+}
+
+// pi/2 split for the reduction: kPio2Hi = RN(pi/2), kPio2Lo = RN(pi/2 - kPio2Hi).
+constexpr double kTwoOverPi = 0.63661977236758134308;
+constexpr double kPio2Hi = 1.5707963267948966;
+constexpr double kPio2Lo = 6.123233995736766e-17;
+
+// fdlibm __kernel_sin / __kernel_cos minimax coefficients on [-pi/4, pi/4].
+constexpr double kS1 = -1.66666666666666324348e-01;
+constexpr double kS2 = 8.33333333332248946124e-03;
+constexpr double kS3 = -1.98412698298579493134e-04;
+constexpr double kS4 = 2.75573137070700676789e-06;
+constexpr double kS5 = -2.50507602534068634195e-08;
+constexpr double kS6 = 1.58969099521155010221e-10;
+constexpr double kC1 = 4.16666666666666019037e-02;
+constexpr double kC2 = -1.38888888888741095749e-03;
+constexpr double kC3 = 2.48015872894767294178e-05;
+constexpr double kC4 = -2.75573143513906633035e-07;
+constexpr double kC5 = 2.08757232129817482790e-09;
+constexpr double kC6 = -1.13596475577881948265e-11;
+
+// (cos x, sin x) for |x| < 2^50.
+UWB_HD void sincos_rd(double x, double* c_out, double* s_out) {
+  const double t = fmad(x, kTwoOverPi, kMagic);
+  const int q = lo_word(t);
+  const double kd = t - kMagic;
+  double r = fmad(kd, -kPio2Hi, x);  // exact (FMA, |result| < 2)
+  r = fmad(kd, -kPio2Lo, r);
+  const double z = r * r;
+  double ps = fmad(kS6, z, kS5);
+  ps = fmad(ps, z, kS4);
+  ps = fmad(ps, z, kS3);
+  ps = fmad(ps, z, kS2);
+  ps = fmad(ps, z, kS1);
+  const double rz = r * z;
+  const double s = fmad(rz, ps, r);
+  double pc = fmad(kC6, z, kC5);
+  pc = fmad(pc, z, kC4);
+  pc = fmad(pc, z, kC3);
+  pc = fmad(pc, z, kC2);
+  pc = fmad(pc, z, kC1);
+  const double zz = z * z;
+  const double c = fmad(zz, pc, fmad(-0.5, z, 1.0));
+  // quadrant: sin(r + q pi/2), cos(r + q pi/2)
+  const bool swap = (q & 1) != 0;
+  double so = swap ? c : s;
+  double co = swap ? s : c;
+  const int sneg = (q & 2) << 30;        // bit 31 if q&2
+  const int cneg = ((q + 1) & 2) << 30;  // bit 31 if (q+1)&2
+  so = from_words(hi_word(so) ^ sneg, lo_word(so));
+  co = from_words(hi_word(co) ^ cneg, lo_word(co));
+  *c_out = co;
+  *s_out = so;
+}
+
+}  // namespace uwb

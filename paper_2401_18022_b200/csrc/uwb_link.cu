@@ -1,0 +1,540 @@
+// Full SNR evaluation on the device: evaluate_link (link_optimizer.hpp:241-245)
+// = build_distance_grid (host, 113 numbers) + Raman ODE (raman_ode.cu) + NLI
+// (nli_kernel.cu) + assemble_link_report (link_optimizer.hpp:194-237, here).
+// Also the C-ABI entry points uwb_power_evolution / uwb_evaluate_link /
+// uwb_evaluate_link_prepare / uwb_evaluate_link_resident.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/uwb_nli.h"
+#include "nli_kernel.cuh"
+#include "raman_ode.cuh"
+#include "uwb_capi_internal.cuh"
+#include "uwb_ctx.cuh"
+#include "uwb_devmath.cuh"
+
+namespace uwb {
+
+namespace {
+
+constexpr double kPlanck = 6.62607015e-34;  // units.hpp:10
+
+struct LinkDev {
+  int n;
+  const double* freq;
+  const double* psd;
+  const uint8_t* guard;
+  double bch;
+  const double* eta;
+  const double* rho_end;
+  const double* nf_db;
+  const int* band;
+  int n_bands;
+  int span_count;
+  int use_snr_trx;
+  double snr_trx;
+  double* out;  // [4n] eta | p_ase | snr_db | capacity, then [3] totals, then [2*n_bands]
+  double* tmp;  // [3n] per-channel p, capacity, log2(1+snr) for the ordered sums
+};
+
+// Per-channel part of assemble_link_report (link_optimizer.hpp:206-224).
+__global__ void link_channels_kernel(LinkDev L) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L.n) return;
+  double* eta_o = L.out;
+  double* pase_o = L.out + L.n;
+  double* snr_o = L.out + 2 * L.n;
+  double* cap_o = L.out + 3 * L.n;
+  eta_o[i] = pase_o[i] = snr_o[i] = cap_o[i] = 0.0;
+  L.tmp[i] = L.tmp[L.n + i] = L.tmp[2 * L.n + i] = 0.0;
+  if (L.guard[i] || L.psd[i] <= 0.0) {
+    L.tmp[i] = -1.0;  // marker: not an active channel
+    return;
+  }
+  const double p = L.psd[i] * L.bch;
+  const double eta = L.eta[i];
+  const double gain = 1.0 / L.rho_end[i];
+  const double nf = L.nf_db[i];
+  // ase_power (link_optimizer.hpp:22-26) with max(gain, 1)
+  const double g1 = gain > 1.0 ? gain : 1.0;
+  const double n_sp = 0.5 * pow(10.0, nf / 10.0);
+  const double pase =
+      static_cast<double>(L.span_count) * (2.0 * n_sp * kPlanck * L.freq[i] * (g1 - 1.0) * L.bch);
+  double denom = eta * p * p * p + pase;
+  if (L.use_snr_trx) denom += p / L.snr_trx;
+  const double snr = p / denom;
+  eta_o[i] = eta;
+  pase_o[i] = pase;
+  snr_o[i] = 10.0 * log10(snr);
+  const double l2 = log2(1.0 + snr);
+  cap_o[i] = 2.0 * L.bch * l2;
+  L.tmp[i] = p;
+  L.tmp[L.n + i] = cap_o[i];
+  L.tmp[2 * L.n + i] = l2;
+}
+
+// Ordered sums (loss, capacity, powers) in channel order (:224-235).
+__global__ void link_totals_kernel(LinkDev L) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double loss = 0.0, cap = 0.0, total_w = 0.0;
+  double* bp = L.out + 4 * L.n + 3;
+  double* bc = bp + L.n_bands;
+  for (int b = 0; b < L.n_bands; ++b) bp[b] = bc[b] = 0.0;
+  for (int i = 0; i < L.n; ++i) {
+    const double p = L.tmp[i];
+    if (p < 0.0) continue;
+    loss -= L.tmp[2 * L.n + i];
+    cap += L.tmp[L.n + i];
+    total_w += p;
+    const int b = L.band ? L.band[i] : -1;
+    if (b >= 0 && b < L.n_bands) {
+      bp[b] += p;
+      bc[b] += L.tmp[L.n + i];
+    }
+  }
+  for (int b = 0; b < L.n_bands; ++b) bp[b] = bp[b] > 0.0 ? 10.0 * log10(bp[b] / 1e-3) : -300.0;
+  L.out[4 * L.n + 0] = loss;
+  L.out[4 * L.n + 1] = cap;
+  L.out[4 * L.n + 2] = total_w > 0.0 ? 10.0 * log10(total_w / 1e-3) : -300.0;
+}
+
+}  // namespace
+
+// build_distance_grid (distance_grid.hpp:23-73), host: 113 numbers.
+int distance_grid_host(double length_m, double density, std::vector<double>* edge,
+                  std::vector<double>* mid, std::vector<double>* width) {
+  if (!(length_m > 0.0)) return fail(UWB_CONFIG_ERROR, "build_distance_grid: length must be > 0");
+  if (!(density > 0.0)) return fail(UWB_CONFIG_ERROR, "build_distance_grid: density must be > 0");
+  long n_edges = std::lround(density * length_m / 1e3) + 1;
+  if (n_edges < 2) n_edges = 2;
+  const size_t n = static_cast<size_t>(n_edges);
+  const double n_steps = static_cast<double>(n - 1);
+  edge->assign(n, 0.0);
+  const double uniform_step = length_m / n_steps;
+  const double first_target = 1e3 / (10.0 * density);
+  if (first_target >= uniform_step * 0.999) {
+    for (size_t i = 0; i < n; ++i) (*edge)[i] = length_m * static_cast<double>(i) / n_steps;
+  } else {
+    auto first_step = [&](double z0) { return z0 * std::expm1(std::log1p(length_m / z0) / n_steps); };
+    double lo = length_m * 1e-12, hi = length_m * 1e12;
+    for (int it = 0; it < 200; ++it) {
+      const double m = std::sqrt(lo * hi);
+      (first_step(m) < first_target ? lo : hi) = m;
+    }
+    const double z0 = std::sqrt(lo * hi);
+    const double t = std::log1p(length_m / z0);
+    for (size_t i = 0; i < n; ++i) (*edge)[i] = z0 * std::expm1(t * static_cast<double>(i) / n_steps);
+  }
+  edge->front() = 0.0;
+  edge->back() = length_m;
+  mid->resize(n - 1);
+  width->resize(n - 1);
+  for (size_t i = 0; i + 1 < n; ++i) {
+    (*mid)[i] = 0.5 * ((*edge)[i] + (*edge)[i + 1]);
+    (*width)[i] = (*edge)[i + 1] - (*edge)[i];
+  }
+  return UWB_OK;
+}
+
+namespace {
+
+template <class T>
+T* up(uwb_ctx* c, DBuf& b, const T* src, size_t n) {
+  T* d = b.get<T>(std::max<size_t>(n, 1));
+  if (d && src && n) cudaMemcpyAsync(d, src, n * sizeof(T), cudaMemcpyHostToDevice, c->stream);
+  return d;
+}
+
+}  // namespace
+
+// Everything evaluate_link keeps resident between calls.
+}  // namespace uwb
+
+struct uwb_ctx::Prepared {
+  int n = 0;
+  int steps = 0;
+  int span_count = 1;
+  int include_raman = 1;
+  double rtol = 1e-9, atol = 1e-16, length = 0.0;
+  uwb_nli_cfg cfg{};
+  uwb::NliParams P{};
+  uwb::FinalizeParams F{};
+  uwb::OdeParams O{};
+  uwb::LinkDev L{};
+  int raman_n = 0;
+  double aeff_ref = 0.0;
+  const double* d_aeff = nullptr;
+  const double* d_rx = nullptr;
+  const double* d_ry = nullptr;
+  double* d_M = nullptr;
+  int* d_lo = nullptr;
+  int* d_hi = nullptr;
+  int* d_status = nullptr;
+  long long* d_rhs = nullptr;
+  double* d_psd = nullptr;  // the NLI/ODE/link read launch PSD from here
+  int grid_ctas = 0;
+  int launches = 0;
+};
+
+namespace uwb {
+
+void release_link_state(uwb_ctx* c) {
+  if (!c->prep) return;
+  delete c->prep;
+  c->prep = nullptr;
+}
+
+namespace {
+
+int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_cfg* lk,
+            const uwb_nli_cfg* cfg) {
+  int rc = validate_grid(g);
+  if (rc) return rc;
+  if (!fb || !lk || !cfg) return fail(UWB_CONFIG_ERROR, "missing fibre / link / solver config");
+  if (!fb->alpha || !fb->aeff || !fb->gamma || !lk->nf_db)
+    return fail(UWB_CONFIG_ERROR, "missing per-channel fibre arrays");
+  if (fb->span_count < 1) return fail(UWB_CONFIG_ERROR, "span count must be >= 1");
+  if (lk->include_raman && (fb->raman_n < 2 || !fb->raman_x || !fb->raman_y))
+    return fail(UWB_CONFIG_ERROR, "raman gain: table needs at least two (x, y) rows");
+  std::vector<double> edge, mid, width;
+  if ((rc = distance_grid_host(fb->length_m, lk->density, &edge, &mid, &width))) return rc;
+  const int steps = static_cast<int>(mid.size());
+  if (steps > kMaxSteps)
+    return fail(UWB_CONFIG_ERROR, "uwb: distance steps per span must be in [1, 256]");
+  const int n = g->n_ch;
+  release_link_state(c);
+  auto* pr = new uwb_ctx::Prepared();
+  c->prep = pr;
+  pr->n = n;
+  pr->steps = steps;
+  pr->span_count = fb->span_count;
+  pr->include_raman = lk->include_raman;
+  pr->rtol = lk->rtol > 0 ? lk->rtol : 1e-9;
+  pr->atol = lk->atol > 0 ? lk->atol : 1e-16;
+  pr->length = fb->length_m;
+  pr->cfg = *cfg;
+  NliParams& P = pr->P;
+  if ((rc = set_cfg(cfg, &P))) return rc;
+
+  // static uploads
+  const double* d_freq = up(c, c->freq, g->freq, n);
+  pr->d_psd = up(c, c->psd, g->psd, n);
+  const uint8_t* d_guard = up(c, c->guard, g->guard, n);
+  const double* d_alpha = up(c, c->alpha, fb->alpha, n);
+  pr->d_aeff = up(c, c->aeff, fb->aeff, n);
+  pr->d_rx = up(c, c->raman_x, fb->raman_x, fb->raman_n);
+  pr->d_ry = up(c, c->raman_y, fb->raman_y, fb->raman_n);
+  pr->raman_n = fb->raman_n;
+  pr->aeff_ref = fb->raman_aeff_ref;
+  const double* d_nf = up(c, c->nf_db, lk->nf_db, n);
+  std::vector<int> band(n, -1);
+  if (lk->band) std::copy(lk->band, lk->band + n, band.begin());
+  const double* d_mid = up(c, c->mid, mid.data(), mid.size());
+  // span-absolute grids: every span is a copy of the one evolution (solve_link_noise :185)
+  std::vector<double> ze, zm, wd, wl;
+  double z_base = 0.0;
+  for (int k = 0; k < fb->span_count; ++k) {
+    for (int m = 0; m <= steps; ++m) ze.push_back(z_base + edge[m]);
+    for (int m = 0; m < steps; ++m) {
+      zm.push_back(z_base + mid[m]);
+      wd.push_back(width[m]);
+    }
+    wl.push_back(width[steps - 1]);
+    z_base += fb->length_m;
+  }
+  P.n_ch = n;
+  P.freq = d_freq;
+  P.psd = pr->d_psd;
+  P.spacing = g->spacing;
+  P.bch = g->bch;
+  P.centre = g->centre;
+  P.half_band = g->half_band;
+  P.n_spans = fb->span_count;
+  P.steps = steps;
+  P.log2rho = c->log2rho.get<double>(static_cast<size_t>(n) * steps);
+  P.span_stride = 0;
+  P.zedge = up(c, c->zedge, ze.data(), ze.size());
+  P.zmid = up(c, c->zmid, zm.data(), zm.size());
+  P.width = up(c, c->width, wd.data(), wd.size());
+  P.wlast = up(c, c->wlast, wl.data(), wl.size());
+  P.beta2 = fb->beta[0];
+  P.beta3 = fb->beta[1];
+  P.beta4 = fb->beta[2];
+
+  // probes: channels with launch power (the resident path keeps this set)
+  std::vector<double> nu, gam;
+  std::vector<int> cp;
+  channel_probes(g, fb->gamma, cfg, c->subset, &nu, &gam, &cp);
+  for (double v : nu)
+    if (std::abs(v - g->centre) > g->half_band)
+      return fail(UWB_CONFIG_ERROR, "quadrant_limits: channel offset must lie inside the half band");
+  const int np = static_cast<int>(nu.size());
+  P.n_probes = np;
+  P.total_rows = np * P.n_q * P.n_r;
+  P.probe_nu = up(c, c->probe_nu, nu.data(), nu.size());
+  P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * steps);
+  P.rowsum = c->rowsum.get<double>(std::max(P.total_rows, 1));
+  P.counter = c->counter.get<unsigned int>(1);
+  P.n_eval = c->n_eval.get<unsigned long long>(1);
+  FinalizeParams& F = pr->F;
+  F.n_probes = np;
+  F.probe_gamma = up(c, c->probe_gamma, gam.data(), gam.size());
+  F.probe_g = c->probe_g.get<double>(std::max(np, 1));
+  F.probe_quad = c->probe_quad.get<double>(4 * std::max(np, 1));
+  F.mirror_q4 = cfg->mirror_q4 ? 1 : 0;
+  F.n_ch = n;
+  F.psd = pr->d_psd;
+  F.bch = g->bch;
+  F.simpson = cfg->simpson ? 1 : 0;
+  F.chan_probe0 = up(c, c->chan_probe0, cp.data(), cp.size());
+  F.eta = c->eta.get<double>(n);
+  F.nli_psd = c->nli_psd.get<double>(n);
+  F.nli_power = c->nli_power.get<double>(n);
+  F.quad = c->quad.get<double>(4 * n);
+  F.skipped = c->skipped.get<uint8_t>(n);
+
+  // ODE
+  OdeParams& O = pr->O;
+  O.n = n;
+  O.alpha = d_alpha;
+  // ode_work: M [n*n] | rho_end [n] | status | rhs | row_lo [n] | row_hi [n] | band [n] | link tmp [3n]
+  const size_t nn = static_cast<size_t>(n) * n;
+  double* w = c->ode_work.get<double>(nn + n + 2 + 3 * n + 3 * n + 8);
+  if (!w) return fail(UWB_CUDA_ERROR, "device allocation failed");
+  pr->d_M = w;
+  O.M = lk->include_raman ? pr->d_M : nullptr;
+  double* d_rho_end = w + nn;
+  pr->d_status = reinterpret_cast<int*>(w + nn + n);
+  pr->d_rhs = reinterpret_cast<long long*>(w + nn + n + 1);
+  int* ip = reinterpret_cast<int*>(w + nn + n + 2);
+  pr->d_lo = ip;
+  pr->d_hi = ip + n;
+  int* d_band2 = ip + 2 * n;
+  double* d_tmp = w + nn + n + 2 + 2 * n;  // 3n ints fit in 1.5n doubles; start tmp after 2n
+  O.row_lo = pr->d_lo;
+  O.row_hi = pr->d_hi;
+  O.steps = steps;
+  O.mid = d_mid;
+  O.length = fb->length_m;
+  O.rtol = pr->rtol;
+  O.atol = pr->atol;
+  O.log2rho = const_cast<double*>(P.log2rho);
+  O.log_rho = nullptr;
+  O.rho_end = d_rho_end;
+  O.status = pr->d_status;
+  O.rhs_evals = pr->d_rhs;
+  cudaMemcpyAsync(d_band2, band.data(), n * sizeof(int), cudaMemcpyHostToDevice, c->stream);
+
+  // assembly
+  LinkDev& L = pr->L;
+  L.n = n;
+  L.freq = d_freq;
+  L.psd = pr->d_psd;
+  L.guard = d_guard;
+  L.bch = g->bch;
+  L.eta = F.eta;
+  L.rho_end = d_rho_end;
+  L.nf_db = d_nf;
+  L.band = d_band2;
+  L.n_bands = std::max(lk->n_bands, 0);
+  L.span_count = fb->span_count;
+  L.use_snr_trx = lk->use_snr_trx;
+  L.snr_trx = lk->use_snr_trx ? std::pow(10.0, lk->snr_trx_db / 10.0) : 0.0;
+  L.out = c->report.get<double>(4 * static_cast<size_t>(n) + 3 + 2 * L.n_bands);
+  L.tmp = d_tmp;
+
+  const int per_sm = nli_ctas_per_sm(steps);
+  if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
+  pr->grid_ctas = c->sm_count * per_sm;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "prepare");
+  return UWB_OK;
+}
+
+// One evaluation on the prepared state; psd_dev = launch PSD (device).
+int run_prepared(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool stats) {
+  uwb_ctx::Prepared* pr = c->prep;
+  int launches = 0;
+  if (psd_dev && psd_dev != pr->d_psd)
+    cudaMemcpyAsync(pr->d_psd, psd_dev, pr->n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  cudaMemsetAsync(pr->d_status, 0, sizeof(int), st);
+  cudaEventRecord(c->ev0, st);
+  const int lo = launch_raman_ode(pr->O, pr->P.freq, pr->d_psd, pr->P.bch, pr->d_aeff, pr->d_rx,
+                                  pr->d_ry, pr->raman_n, pr->aeff_ref, pr->d_M, pr->d_lo,
+                                  pr->d_hi, st);
+  if (lo < 0) return fail(UWB_CUDA_ERROR, "raman ODE launch failed (cluster/smem)");
+  launches += lo;
+  if (pr->P.n_probes > 0) {
+    const int ln = launch_nli(pr->P, pr->F, pr->grid_ctas, st, stats ? c->evk0 : nullptr,
+                              stats ? c->evk1 : nullptr);
+    if (ln < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
+    launches += ln;
+  } else {
+    launches += launch_finalize_channels_only(pr->F, st);
+  }
+  LinkDev L = pr->L;
+  link_channels_kernel<<<(L.n + 127) / 128, 128, 0, st>>>(L);
+  link_totals_kernel<<<1, 32, 0, st>>>(L);
+  launches += 2;
+  cudaEventRecord(c->ev1, st);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "evaluate_link launch");
+  c->last_launches = launches;
+  return UWB_OK;
+}
+
+int check_status(uwb_ctx* c) {
+  int status = 0;
+  cudaMemcpy(&status, c->prep->d_status, sizeof(int), cudaMemcpyDeviceToHost);
+  switch (status) {
+    case 0: return UWB_OK;
+    case 1: return fail(UWB_SOLVER_ERROR, "power evolution: non-positive rho");
+    case 2: return fail(UWB_SOLVER_ERROR, "rk45: step budget exhausted");
+    default: return fail(UWB_SOLVER_ERROR, "rk45: step size underflow");
+  }
+}
+
+}  // namespace
+}  // namespace uwb
+
+using namespace uwb;
+
+extern "C" {
+
+int uwb_evaluate_link_prepare(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
+                              const uwb_link_cfg* link, const uwb_nli_cfg* cfg) {
+  if (!c) return fail(UWB_CONFIG_ERROR, "null context");
+  cudaSetDevice(c->device);
+  return prepare(c, grid, fibre, link, cfg);
+}
+
+int uwb_evaluate_link_resident(uwb_ctx* c, const double* psd_dev, double* report_dev,
+                               void* stream) {
+  if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+  int rc = run_prepared(c, psd_dev, st, false);
+  if (rc) return rc;
+  if (report_dev) {
+    const size_t cnt = 4 * static_cast<size_t>(c->prep->n) + 3 + 2 * c->prep->L.n_bands;
+    cudaMemcpyAsync(report_dev, c->prep->L.out, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  }
+  return UWB_OK;
+}
+
+int uwb_evaluate_link(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
+                      const uwb_link_cfg* link, const uwb_nli_cfg* cfg, uwb_link_report* out) {
+  if (!c) return fail(UWB_CONFIG_ERROR, "null context");
+  cudaSetDevice(c->device);
+  int rc = prepare(c, grid, fibre, link, cfg);
+  if (rc) return rc;
+  uwb_ctx::Prepared* pr = c->prep;
+  if ((rc = run_prepared(c, nullptr, c->stream, true))) return rc;
+  const int n = pr->n;
+  cudaStream_t st = c->stream;
+  std::vector<double> rep(4 * static_cast<size_t>(n) + 3 + 2 * pr->L.n_bands);
+  cudaMemcpyAsync(rep.data(), pr->L.out, rep.size() * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (out && out->rho_end)
+    cudaMemcpyAsync(out->rho_end, pr->O.rho_end, n * sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "evaluate_link");
+  if ((rc = check_status(c))) return rc;
+  if (out) {
+    if (out->eta) std::memcpy(out->eta, rep.data(), n * sizeof(double));
+    if (out->p_ase) std::memcpy(out->p_ase, rep.data() + n, n * sizeof(double));
+    if (out->snr_db) std::memcpy(out->snr_db, rep.data() + 2 * n, n * sizeof(double));
+    if (out->capacity) std::memcpy(out->capacity, rep.data() + 3 * n, n * sizeof(double));
+    out->loss_value = rep[4 * n];
+    out->total_capacity = rep[4 * n + 1];
+    out->total_power_dbm = rep[4 * n + 2];
+    const int nb = pr->L.n_bands;
+    if (out->band_power_dbm) std::memcpy(out->band_power_dbm, rep.data() + 4 * n + 3, nb * 8);
+    if (out->band_capacity) std::memcpy(out->band_capacity, rep.data() + 4 * n + 3 + nb, nb * 8);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    out->elapsed_seconds = ms * 1e-3;
+    float kms = 0.f;
+    if (pr->P.n_probes > 0) cudaEventElapsedTime(&kms, c->ev0, c->evk0);
+    out->ode_seconds = kms * 1e-3;
+  }
+  if (pr->P.n_probes > 0) {
+    float kms = 0.f;
+    cudaEventElapsedTime(&kms, c->evk0, c->evk1);
+    c->last_kernel_ms = kms;
+    unsigned long long ne = 0;
+    cudaMemcpy(&ne, pr->P.n_eval, sizeof ne, cudaMemcpyDeviceToHost);
+    c->last_points = static_cast<double>(ne);
+    c->last_inner_steps = static_cast<double>(ne) * pr->P.steps * pr->P.n_spans;
+  }
+  return UWB_OK;
+}
+
+int uwb_power_evolution(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
+                        const uwb_link_cfg* link, int steps, const double* mid, double* log_rho,
+                        double* rho_end) {
+  if (!c) return fail(UWB_CONFIG_ERROR, "null context");
+  cudaSetDevice(c->device);
+  release_link_state(c);  // shares buffers with the prepared evaluation
+  int rc = validate_grid(grid);
+  if (rc) return rc;
+  if (!fibre || !link || !fibre->alpha || !fibre->aeff)
+    return fail(UWB_CONFIG_ERROR, "missing fibre arrays");
+  if (steps < 1 || !mid) return fail(UWB_CONFIG_ERROR, "distance grid has no steps");
+  const int n = grid->n_ch;
+  cudaStream_t st = c->stream;
+  const double* d_freq = up(c, c->freq, grid->freq, n);
+  const double* d_psd = up(c, c->psd, grid->psd, n);
+  const double* d_alpha = up(c, c->alpha, fibre->alpha, n);
+  const double* d_aeff = up(c, c->aeff, fibre->aeff, n);
+  const double* d_rx = up(c, c->raman_x, fibre->raman_x, fibre->raman_n);
+  const double* d_ry = up(c, c->raman_y, fibre->raman_y, fibre->raman_n);
+  const double* d_mid = up(c, c->mid, mid, steps);
+  const size_t nn = static_cast<size_t>(n) * n;
+  double* w = c->ode_work.get<double>(nn + 2 * static_cast<size_t>(n) * steps + n + 2 + 2 * n);
+  if (!w) return fail(UWB_CUDA_ERROR, "device allocation failed");
+  OdeParams O{};
+  O.n = n;
+  O.alpha = d_alpha;
+  O.M = link->include_raman ? w : nullptr;
+  double* d_l2 = w + nn;
+  double* d_ln = d_l2 + static_cast<size_t>(n) * steps;
+  double* d_re = d_ln + static_cast<size_t>(n) * steps;
+  int* d_status = reinterpret_cast<int*>(d_re + n);
+  long long* d_rhs = reinterpret_cast<long long*>(d_re + n + 1);
+  int* d_lo = reinterpret_cast<int*>(d_re + n + 2);
+  O.row_lo = d_lo;
+  O.row_hi = d_lo + n;
+  O.steps = steps;
+  O.mid = d_mid;
+  O.length = fibre->length_m;
+  O.rtol = link->rtol > 0 ? link->rtol : 1e-9;
+  O.atol = link->atol > 0 ? link->atol : 1e-16;
+  O.log2rho = d_l2;
+  O.log_rho = d_ln;
+  O.rho_end = d_re;
+  O.status = d_status;
+  O.rhs_evals = d_rhs;
+  if (fibre->raman_n < 2 && link->include_raman)
+    return fail(UWB_CONFIG_ERROR, "raman gain: table needs at least two (x, y) rows");
+  cudaMemsetAsync(d_status, 0, sizeof(int), st);
+  const int lo = launch_raman_ode(O, d_freq, d_psd, grid->bch, d_aeff, d_rx, d_ry, fibre->raman_n,
+                                  fibre->raman_aeff_ref, w, d_lo, d_lo + n, st);
+  if (lo < 0) return fail(UWB_CUDA_ERROR, "raman ODE launch failed (cluster/smem)");
+  c->last_launches = lo;
+  if (log_rho) cudaMemcpyAsync(log_rho, d_ln, static_cast<size_t>(n) * steps * 8, cudaMemcpyDeviceToHost, st);
+  if (rho_end) cudaMemcpyAsync(rho_end, d_re, n * 8, cudaMemcpyDeviceToHost, st);
+  int status = 0;
+  cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "power evolution");
+  if (status == 1) return fail(UWB_SOLVER_ERROR, "power evolution: non-positive rho");
+  if (status == 2) return fail(UWB_SOLVER_ERROR, "rk45: step budget exhausted");
+  if (status) return fail(UWB_SOLVER_ERROR, "rk45: step size underflow");
+  return UWB_OK;
+}
+
+}  // extern "C"

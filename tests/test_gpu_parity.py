@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (libuwbnli.so through the C-ABI) against the
+reference's own outputs (tests/golden, generated from the unmodified
+reference headers) and the C oracle on the same inputs.
+
+Tolerances (BASELINE.json north_star: <= 1e-6 relative eta, <= 0.01 dB SNR):
+  NLI on identical inputs ............ 1e-9 relative (FP64; observed ~1e-13)
+  full path (device ODE + NLI + SNR) . 1e-6 relative eta, 0.01 dB SNR
+"""
+import numpy as np
+import pytest
+
+import paper_2401_18022_b200 as uwb
+from helpers import cfg_of, engine_inputs_from_oracle, product_scenario, to_db
+from pyoracle import Case, toy_case
+
+pytestmark = pytest.mark.gpu
+
+NLI_TOL = 1e-9
+
+SMALL_CASES = ["cband11", "oband11", "oband11_simpson", "cband11_nr40", "cband11_uniform",
+               "cband11_direct_q4", "toy5_nr64", "toy5_guard", "toy5_simpson", "toy5_2mw",
+               "toy3_3span", "cband11_uniform_z", "uwb589_random_launch"]
+
+
+def _rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    den = np.where(b == 0, 1.0, np.abs(b))
+    return float(np.max(np.abs(a - b) / den)) if a.size else 0.0
+
+
+@pytest.mark.parametrize("name", SMALL_CASES + ["uwb589_75_0.95", "uwb589_150_1.4"])
+def test_all_channels_nli_matches_reference(name, golden, oracle, engine):
+    rec = golden["all_channels_nli"][name]
+    case = Case.from_json(rec["case"])
+    prep = oracle.prepare(case)
+    grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
+    r = uwb.all_channels_nli(grid, spans, betas, None, cfg_of(case), engine=engine, gamma=gamma)
+    assert np.array_equal(r.skipped, np.array(rec["skipped"], np.uint8))
+    assert _rel(r.eta, rec["eta"]) < NLI_TOL
+    assert _rel(r.nli_psd, rec["nli_psd"]) < NLI_TOL
+    assert _rel(r.nli_power, rec["nli_power"]) < NLI_TOL
+    q = np.array(rec["quadrant"])
+    assert _rel(r.quadrant, q) < NLI_TOL
+    assert r.elapsed_seconds > 0.0
+
+
+def test_nli_psd_at_and_cartesian(golden, oracle, engine):
+    for rec in golden["nli_psd_at"]:
+        case = Case.from_json(rec["case"])
+        prep = oracle.prepare(case)
+        grid, spans, betas, _ = engine_inputs_from_oracle(prep, case.density)
+        q = np.zeros(4)
+        v = uwb.nli_psd_at(grid, spans, betas, rec["gamma"], cfg_of(case), rec["nu"],
+                           quadrant_diag=q, engine=engine)
+        assert abs(v / rec["value"] - 1.0) < NLI_TOL
+        assert _rel(q, rec["quad"]) < NLI_TOL
+        if "cartesian600" in rec:  # test_gn_integral.cpp:226-235
+            assert abs(to_db(v / rec["cartesian600"])) < 0.1
+
+
+def test_mirror_q4_equals_direct_q4(oracle, engine):
+    """test_gn_integral.cpp:250-263 on the device."""
+    case = toy_case(3, n_r=80)
+    prep = oracle.prepare(case)
+    grid, spans, betas, _ = engine_inputs_from_oracle(prep, case.density)
+    qa, qb = np.zeros(4), np.zeros(4)
+    nu = grid.freq[0]
+    a = uwb.nli_psd_at(grid, spans, betas, 1.3e-3, cfg_of(case), nu, quadrant_diag=qa, engine=engine)
+    direct = cfg_of(case)
+    direct.mirror_q4 = False
+    b = uwb.nli_psd_at(grid, spans, betas, 1.3e-3, direct, nu, quadrant_diag=qb, engine=engine)
+    assert a == pytest.approx(b, rel=1e-12)
+    assert qa[3] == pytest.approx(qb[3], rel=1e-12)
+    assert qb[1] == pytest.approx(qb[3], rel=1e-12)
+
+
+def test_batched_probes_equal_single_probes(oracle, engine):
+    case = toy_case(5, n_r=40)
+    prep = oracle.prepare(case)
+    grid, spans, betas, _ = engine_inputs_from_oracle(prep, case.density)
+    nus = grid.freq.copy()
+    batch = uwb.nli_psd_at(grid, spans, betas, np.full(5, 1.3e-3), cfg_of(case), nus, engine=engine)
+    for k, nu in enumerate(nus):
+        single = uwb.nli_psd_at(grid, spans, betas, 1.3e-3, cfg_of(case), float(nu), engine=engine)
+        assert single == batch[k]  # bit-identical: per-probe reductions are order-fixed
+
+
+def test_channel_nli_simpson(oracle, engine):
+    case = toy_case(5, n_r=64, simpson=1)
+    prep = oracle.prepare(case)
+    grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
+    ref = oracle.all_channels_nli(case, prep)
+    for ch in range(5):
+        v = uwb.channel_nli(grid, spans, betas, gamma[ch], cfg_of(case), ch, engine=engine)
+        assert v == pytest.approx(ref["nli_psd"][ch], rel=NLI_TOL)
+
+
+def test_deterministic_and_partition_independent(golden, oracle, engine):
+    """Bit-identity across worker counts (test_gn_integral.cpp:291-300) becomes
+    bit-identity across runs and across channel partitions (multi-GPU)."""
+    case = Case.from_json(golden["all_channels_nli"]["cband11_nr40"]["case"])
+    prep = oracle.prepare(case)
+    grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
+    cfg = cfg_of(case)
+    a = uwb.all_channels_nli(grid, spans, betas, None, cfg, engine=engine, gamma=gamma)
+    b = uwb.all_channels_nli(grid, spans, betas, None, cfg, engine=engine, gamma=gamma)
+    assert np.array_equal(a.eta, b.eta) and np.array_equal(a.quadrant, b.quadrant)
+    merged = np.zeros_like(a.eta)
+    for part in (np.arange(0, 11, 2), np.arange(1, 11, 2)):
+        engine.set_channel_subset(part)
+        r = uwb.all_channels_nli(grid, spans, betas, None, cfg, engine=engine, gamma=gamma)
+        merged[part] = r.eta[part]
+        others = np.setdiff1d(np.arange(11), part)
+        assert np.all(r.skipped[others] == 1) and np.all(r.eta[others] == 0.0)
+    engine.set_channel_subset(None)
+    assert np.array_equal(merged, a.eta)
+
+
+def test_cubic_power_scaling(oracle, engine):
+    """test_gn_integral.cpp:277-289 / acceptance C4: Raman off, +3 dB -> +9 dB."""
+    base = toy_case(5, n_r=64)
+    loud = toy_case(5, n_r=64, uniform_w=2e-3)
+    out = []
+    for case in (base, loud):
+        prep = oracle.prepare(case)
+        grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
+        out.append(uwb.all_channels_nli(grid, spans, betas, None, cfg_of(case), engine=engine,
+                                        gamma=gamma))
+    assert np.all(out[0].eta > 0)
+    np.testing.assert_allclose(out[1].nli_power, 8.0 * out[0].nli_power, rtol=1e-9)
+    np.testing.assert_allclose(out[1].eta, out[0].eta, rtol=1e-9)
+
+
+def test_config_errors(oracle, engine):
+    """test_gn_integral.cpp:339-346: ConfigError contract."""
+    case = toy_case(5, n_r=64)
+    prep = oracle.prepare(case)
+    grid, spans, betas, _ = engine_inputs_from_oracle(prep, case.density)
+    bad = cfg_of(case)
+    bad.n_r = 1
+    with pytest.raises(uwb.ConfigError):
+        uwb.nli_psd_at(grid, spans, betas, 1e-3, bad, grid.centre, engine=engine)
+    with pytest.raises(uwb.ConfigError):
+        uwb.nli_psd_at(grid, [], betas, 1e-3, cfg_of(case), grid.centre, engine=engine)
+    other = uwb.make_uniform_grid(4, 12e9, 10e9, 193.5e12)
+    with pytest.raises(uwb.ConfigError):
+        uwb.nli_psd_at(other, spans, betas, 1e-3, cfg_of(case), other.centre, engine=engine)
+    with pytest.raises(uwb.ConfigError):  # quadrant_limits: probe outside the half band
+        uwb.nli_psd_at(grid, spans, betas, 1e-3, cfg_of(case), grid.centre + 2 * grid.half_band,
+                       engine=engine)
+
+
+def test_dark_grid_reports_zeros(oracle, engine):
+    case = toy_case(5, n_r=64)
+    prep = oracle.prepare(case)
+    grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
+    grid.psd[:] = 0.0
+    grid.guard[:] = 1
+    r = uwb.all_channels_nli(grid, spans, betas, None, cfg_of(case), engine=engine, gamma=gamma)
+    assert np.all(r.skipped == 1) and np.all(r.eta == 0.0)
+
+
+# ---------------------------------------------------------------- device ODE
+@pytest.mark.parametrize("name", ["cband11", "oband11", "toy3", "toy3_lossless", "uwb589",
+                                  "uwb589_2dbm", "uwb589_random_launch"])
+def test_power_evolution_matches_reference(name, golden, engine):
+    rec = golden["power_evolution"][name]
+    case = Case.from_json(rec["case"])
+    grid, fibre = product_scenario(case)
+    zg = uwb.build_distance_grid(case.length_m, case.density)
+    evo = uwb.solve_power_evolution(fibre, grid, zg, uwb.RamanSolveOptions(bool(case.raman)),
+                                    engine=engine)
+    assert evo.steps() == rec["steps"]
+    np.testing.assert_allclose(evo.rho_end, rec["rho_end"], rtol=1e-9)
+    if "log_rho" in rec:
+        np.testing.assert_allclose(evo.log_rho, rec["log_rho"], rtol=0, atol=1e-9)
+    for i, v in rec["log_rho_samples"]:
+        assert abs(evo.log_rho[i] - v) < 1e-9
+    assert abs(np.sum(evo.log_rho) - rec["log_rho_sum"]) < 1e-6
+
+
+# ---------------------------------------------------------------- full SNR evaluation
+@pytest.mark.parametrize("name", ["uwb589_75_0.95", "uwb589_random_launch"])
+def test_evaluate_link_matches_reference(name, golden, engine):
+    rec = golden["evaluate_link"][name]
+    case = Case.from_json(rec["case"])
+    grid, fibre = product_scenario(case)
+    lc = uwb.LinkConfig(gn=cfg_of(case), raman=uwb.RamanSolveOptions(bool(case.raman)))
+    rep = uwb.evaluate_link(fibre, grid, lc, engine=engine)
+    eta_ref = np.array(rec["eta"])
+    act = eta_ref > 0
+    assert _rel(rep.eta[act], eta_ref[act]) < 1e-6
+    assert np.max(np.abs(rep.snr_db[act] - np.array(rec["snr_db"])[act])) < 0.01
+    np.testing.assert_allclose(rep.p_ase[act], np.array(rec["p_ase"])[act], rtol=1e-6)
+    assert rep.loss_value == pytest.approx(rec["loss"], rel=1e-9)
+    assert rep.total_capacity == pytest.approx(rec["total_capacity"], rel=1e-9)
+    assert rep.total_power_dbm == pytest.approx(rec["total_power_dbm"], abs=1e-9)
+
+
+def test_resident_link_equals_host_call(golden, engine):
+    import torch
+
+    rec = golden["evaluate_link"]["uwb589_random_launch"]
+    case = Case.from_json(rec["case"])
+    grid, fibre = product_scenario(case)
+    lc = uwb.LinkConfig(gn=cfg_of(case))
+    host = uwb.evaluate_link(fibre, grid, lc, engine=engine)
+    res = uwb.ResidentLink(fibre, grid, lc, engine=engine)
+    psd = torch.tensor(grid.psd, dtype=torch.float64, device="cuda:0")
+    out = torch.zeros(res.report_len, dtype=torch.float64, device="cuda:0")
+    res.run(psd.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    n = grid.size()
+    assert np.array_equal(o[:n], host.eta)
+    assert np.array_equal(o[2 * n:3 * n], host.snr_db)
+    assert o[4 * n] == host.loss_value
