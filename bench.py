@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""bench.py — seconds per full-band SNR evaluation (589 x 96 GBd O->U band,
+80 km SSMF, ISRS on) on 1..N B200s, BASELINE.json's metric.
+
+One step = one full SNR evaluation = evaluate_link (link_optimizer.hpp:241):
+Raman power-evolution ODE + ISRS-GN NLI of every active channel + SNR
+assembly, at the accurate setting N_R = 150, N_M density 1.4 /km (SURVEY §8d
+config 3; the paper's < 0.1 dB setting).  Lower is better.
+
+  value : device time per evaluation, inputs (launch PSDs) resident in HBM,
+          CUDA events on the launching stream, max over ranks, L2 flushed
+          (256 MiB write) between timed steps.
+  e2e   : the same evaluation through the public API with HOST buffers
+          (uwb.evaluate_link at N=1: host grid/fibre arrays in, host report
+          out; host<->device copies and host prep inside the timed region).
+
+N > 1 (torchrun, one rank per GPU, NCCL): active channels are dealt
+round-robin to ranks (no data-path collective inside the NLI); each rank runs
+the ODE (replicated, tiny inputs) and the NLI of its channels, one NCCL
+all-reduce (sum) assembles the eta vector, then the SNR report.  Total work is
+fixed as N grows: "scaling": "strong".
+
+--impl reference: rank 0 times the reference's own CPU implementation
+(oracle/_ref/libuwbref.so = the unmodified uwblink headers compiled here;
+the C restatement oracle/liboracle.so if absent) on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "s per full-band SNR eval (589x96GBaud, 80km)"
+UNIT = "s"
+FLOPS_PER_STEP = 87.0  # SURVEY §8(d) frozen convention, FP64 flops per inner phasor step
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    p.add_argument("--n-r", type=int, default=150)
+    p.add_argument("--density", type=float, default=1.4)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-variants", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def config(args, world):
+    return {"workload": "589ch x 96GBd O-U band (1260-1675 nm), 80 km SSMF x1 span, 0 dBm/ch, "
+                        "ISRS on; full SNR eval = Raman ODE + GN-integral NLI + SNR",
+            "channels": 589, "active_channels": 557, "n_r": args.n_r,
+            "step_density_per_km": args.density, "u1_sampling": "log", "mirror_q4": True,
+            "parallelism": f"coi-partition x{world}" if world > 1 else "single-gpu",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap,power.draw",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- CPU reference
+def reference_eval_fn(n_r, density):
+    """One reference evaluate_link on all host cores; returns (fn, kind)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Oracle, RefLib, uwb589
+
+    case = uwb589(n_r=n_r, density=density, workers=0)
+    if RefLib.available():
+        R = RefLib()
+        return (lambda: R.evaluate_link(case)), "reference"
+    O = Oracle()
+    return (lambda: O.evaluate_link(case)), "port"
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    fn, kind = reference_eval_fn(args.n_r, args.density)
+    # each step is one full evaluation (~5-10 s on 8-16 host cores): bound the run
+    steps = max(1, min(args.steps, 5))
+    warm = min(args.warmup, 1)
+    for _ in range(warm):
+        fn()
+    ts, parts = [], []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        r = fn()
+        ts.append(time.perf_counter() - t0)
+        parts.append((r.get("t_ode", 0.0), r.get("t_nli", 0.0)))
+    v = float(np.mean(ts))
+    cores = os.cpu_count()
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": steps, "warmup": warm, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config(args, 1),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": f"{steps} full evaluate_link calls (ODE+NLI+SNR), "
+                                       f"workers=all {cores} host threads",
+                             "ode_s": float(np.mean([p[0] for p in parts])),
+                             "nli_s": float(np.mean([p[1] for p in parts]))},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- engine
+def read_traffic():
+    p = os.path.join(ROOT, "profiles", "nli_traffic.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh)
+    return None
+
+
+def run_engine(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2401_18022_b200 as uwb
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    eng = uwb.Engine(local)
+    peak = eng.fp64_peak_tflops()
+
+    grid = uwb.make_default_uwb_grid()
+    uwb.set_uniform_launch(grid, 1e-3)
+    fibre = uwb.default_fibre()
+    gn = uwb.GnSolverConfig(n_r=args.n_r, mean_step_density=args.density)
+    lc = uwb.LinkConfig(gn=gn)
+    active = np.flatnonzero((grid.guard == 0) & (grid.psd > 0))
+    mine = active[rank::world] if world > 1 else None
+    if mine is not None:
+        eng.set_channel_subset(mine)
+
+    # a real (non-legacy) stream: the C-ABI maps a NULL stream to its own
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    sp = stream.cuda_stream
+    res = uwb.ResidentLink(fibre, grid, lc, engine=eng)
+    psd = torch.tensor(grid.psd, dtype=torch.float64, device=dev)
+    report = torch.zeros(res.report_len, dtype=torch.float64, device=dev)
+    eta_ptr, n_ch = res.eta_buffer()
+
+    class _Cai:  # zero-copy torch view of the engine's eta buffer for NCCL
+        __cuda_array_interface__ = {"shape": (n_ch,), "typestr": "<f8", "data": (eta_ptr, False),
+                                    "version": 3}
+
+    eta_view = torch.as_tensor(_Cai(), device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        if world == 1:
+            res.run(psd.data_ptr(), report.data_ptr(), sp)
+        else:
+            res.run_noise(psd.data_ptr(), sp)
+            dist.all_reduce(eta_view, op=dist.ReduceOp.SUM)
+            res.run_report(report.data_ptr(), sp)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+    res.check_status()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    kern_ms = []
+    launches = 0
+    barrier()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+            torch.cuda.synchronize(dev)
+            launches += eng.last_launches() + (2 if world > 1 else 0)
+            kern_ms.append(eng.last_nli_stats()["kernel_ms"])
+        barrier()
+    res.check_status()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(np.sum(step_ms))
+    stats = eng.last_nli_stats()
+    t = torch.tensor([total_ms, float(np.mean(kern_ms)), stats["inner_steps"]], dtype=torch.float64,
+                     device=dev)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax[:2], op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum[2:], op=dist.ReduceOp.SUM)
+        total_ms, kmax, inner = float(tmax[0]), float(tmax[1]), float(tsum[2])
+    else:
+        kmax, inner = float(t[1]), float(t[2])
+    ms_per = total_ms / args.steps
+    rep = report.cpu().numpy()
+    n = grid.size()
+
+    # ---- e2e through the public API with host buffers
+    e2e_ms, h2d, d2h = None, 0, 0
+    if world == 1:
+        for _ in range(2):
+            uwb.evaluate_link(fibre, grid, lc, engine=eng)
+        ts = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            r = uwb.evaluate_link(fibre, grid, lc, engine=eng)
+            ts.append(time.perf_counter() - t0)
+        e2e_ms = float(np.mean(ts)) * 1e3
+        h2d, d2h = eng.last_transfer_bytes()
+        assert np.array_equal(r.eta, rep[:n]), "e2e and resident paths disagree"
+    else:
+        # host-buffer variant of the split path: pinned H2D of the launch PSDs,
+        # noise, NCCL all-reduce, report, pinned D2H of the report
+        hp = torch.tensor(grid.psd, dtype=torch.float64).pin_memory()
+        hr = torch.empty(res.report_len, dtype=torch.float64).pin_memory()
+        ts = []
+        barrier()
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            t0 = time.perf_counter()
+            psd.copy_(hp, non_blocking=True)
+            step()
+            hr.copy_(report, non_blocking=True)
+            torch.cuda.synchronize(dev)
+            ts.append(time.perf_counter() - t0)
+        tt = torch.tensor([float(np.mean(ts))], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt[0]) * 1e3
+        h2d, d2h = n * 8, res.report_len * 8
+
+    # ---- alternative settings (paper-speed 75/0.95), value only
+    variants = {}
+    if not args.no_variants and world == 1:
+        for nr, dens in ((75, 0.95),):
+            gv = uwb.GnSolverConfig(n_r=nr, mean_step_density=dens)
+            rv = uwb.ResidentLink(fibre, grid, uwb.LinkConfig(gn=gv), engine=eng)
+            rv.run(psd.data_ptr(), report.data_ptr(), sp)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            vs = []
+            for _ in range(5):
+                flush.zero_()
+                e0.record(stream)
+                rv.run(psd.data_ptr(), report.data_ptr(), sp)
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                vs.append(e0.elapsed_time(e1))
+            variants[f"n_r{nr}_density{dens}"] = {"s_per_eval": float(np.median(vs)) / 1e3}
+
+    # ---- CPU reference beside it (rank 0, N=1)
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            fn, kind = reference_eval_fn(args.n_r, args.density)
+            t0 = time.perf_counter()
+            r = fn()
+            v = time.perf_counter() - t0
+            cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
+                   "sample": "1 full evaluate_link (ODE+NLI+SNR) of the same workload, "
+                             f"workers = all {os.cpu_count()} host threads",
+                   "ode_s": r.get("t_ode"), "nli_s": r.get("t_nli")}
+        except Exception as e:  # the baseline is reported, never the product
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        achieved = FLOPS_PER_STEP * inner / (kmax * 1e-3) / 1e12 if kmax > 0 else None
+        tr = read_traffic()
+        line = {
+            "metric": METRIC, "value": ms_per / 1e3, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (built-in fibre model + 589-ch band plan; no external data)",
+            "config": config(args, world),
+            "e2e": {"value": e2e_ms / 1e3, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "api": "uwb.evaluate_link -> uwb_evaluate_link (C-ABI), host in/out"
+                    if world == 1 else "pinned H2D + resident noise/all-reduce/report + D2H"},
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if achieved else None,
+                         "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                         "kernel": "nli_rows_kernel (GN integrand)",
+                         "kernel_ms": kmax, "inner_steps": inner,
+                         "flops_per_step": FLOPS_PER_STEP,
+                         "peak_source": "live DFMA microbenchmark (uwb_fp64_peak), this GPU",
+                         "kernel_share_of_step": kmax / ms_per if ms_per else None},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+            "variants": variants,
+            "result_check": {"loss": float(rep[4 * n]), "total_capacity_tbps": float(rep[4 * n + 1]) / 1e12},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    eng.close()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_engine(args)
+
+
+if __name__ == "__main__":
+    main()

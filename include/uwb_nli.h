@@ -188,6 +188,19 @@ int uwb_evaluate_link_prepare(uwb_ctx* ctx, const uwb_grid* grid, const uwb_fibr
                               const uwb_link_cfg* link, const uwb_nli_cfg* cfg);
 int uwb_evaluate_link_resident(uwb_ctx* ctx, const double* psd_dev, double* report_dev,
                                void* stream);
+/* Split resident evaluation for multi-GPU runs: the noise stage (Raman ODE +
+ * NLI of this context's channel subset) leaves eta in the buffer returned by
+ * uwb_link_eta_buffer (zeros outside the subset); the caller all-reduces it
+ * across ranks (NCCL), then the report stage assembles SNR from the full eta.
+ * uwb_resident_status synchronises and maps the ODE status to SolverError. */
+int uwb_evaluate_link_resident_noise(uwb_ctx* ctx, const double* psd_dev, void* stream);
+int uwb_evaluate_link_resident_report(uwb_ctx* ctx, double* report_dev, void* stream);
+int uwb_link_eta_buffer(uwb_ctx* ctx, double** eta_dev, int* n_ch);
+int uwb_resident_status(uwb_ctx* ctx);
+/* Host<->device bytes moved by the last public call. */
+int uwb_last_transfer_bytes(uwb_ctx* ctx, unsigned long long* h2d, unsigned long long* d2h);
+/* Live FP64 FMA-pipe peak of this device, TFLOP/s (roofline denominator). */
+int uwb_fp64_peak(uwb_ctx* ctx, double* tflops);
 /* Kernel launches issued by the last call (evidence for bench gpu_launches). */
 int uwb_last_launch_count(uwb_ctx* ctx);
 /* Device time (ms) of the last NLI integrand kernel and its inner-step count

@@ -111,6 +111,13 @@ SIGNATURES = {
     "uwb_evaluate_link_prepare": (C.c_int, [C.c_void_p, C.POINTER(Grid), C.POINTER(Fibre),
                                             C.POINTER(LinkCfg), C.POINTER(NliCfg)]),
     "uwb_evaluate_link_resident": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "uwb_evaluate_link_resident_noise": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "uwb_evaluate_link_resident_report": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "uwb_link_eta_buffer": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), IP]),
+    "uwb_resident_status": (C.c_int, [C.c_void_p]),
+    "uwb_last_transfer_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_ulonglong),
+                                          C.POINTER(C.c_ulonglong)]),
+    "uwb_fp64_peak": (C.c_int, [C.c_void_p, DP]),
     "uwb_last_launch_count": (C.c_int, [C.c_void_p]),
     "uwb_last_nli_stats": (C.c_int, [C.c_void_p, DP, DP, DP]),
     "uwb_model_fibre": (C.c_int, [C.c_int, C.c_double, C.c_int, DP, C.c_double,

@@ -29,6 +29,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <algorithm>
 #include <cstdio>
 
 #include "nli_kernel.cuh"
@@ -41,7 +42,7 @@ namespace {
 constexpr int kWarps = 8;  // warps per CTA
 constexpr unsigned kFull = 0xffffffffu;
 
-__constant__ double c_exp2_tab[32] = UWB_EXP2_TABLE;
+__constant__ double c_exp2_tab16[16] = UWB_EXP2_TABLE16;
 
 // ChannelGrid::psd_at (channel_grid.hpp:35-42) fused with stencil_for
 // (gn_integral.hpp:110-129): both start from the same `pos`.
@@ -50,30 +51,26 @@ struct Stencil {
   double hw0, hw1;
 };
 
-__device__ __forceinline__ double psd_and_stencil(const NliParams& P, double nu, Stencil* s) {
+__device__ __forceinline__ Stencil psd_and_stencil(const NliParams& P, double nu, double* psd) {
   const double pos = (nu - P.freq[0]) / P.spacing;
-  double psd = 0.0;
   const long i = lround(pos);
+  double v = 0.0;
   if (i >= 0 && i < P.n_ch) {
-    if (!(fabs(nu - __ldg(P.freq + i)) > 0.5 * P.bch)) psd = __ldg(P.psd + i);
+    if (!(fabs(nu - __ldg(P.freq + i)) > 0.5 * P.bch)) v = __ldg(P.psd + i);
   }
-  s->i0 = 0;
-  s->i1 = 0;
-  s->hw0 = 0.5;
-  s->hw1 = 0.0;
+  *psd = v;
   const int n = P.n_ch;
-  if (n == 1 || pos <= 0.0) return psd;
-  if (pos >= static_cast<double>(n - 1)) {
-    s->i0 = s->i1 = n - 1;
-    return psd;
-  }
-  const int k = static_cast<int>(pos);  // pos in (0, n-1): truncation == size_t cast
+  // stencil_for: clamp below (pos <= 0) / above (pos >= n-1), else linear
+  const bool below = n == 1 || pos <= 0.0;
+  const bool above = !below && pos >= static_cast<double>(n - 1);
+  const int k = (below || above) ? 0 : static_cast<int>(pos);  // truncation == size_t cast
   const double t = pos - static_cast<double>(k);
-  s->i0 = k;
-  s->i1 = k + 1;
-  s->hw0 = 0.5 * (1.0 - t);
-  s->hw1 = 0.5 * t;
-  return psd;
+  Stencil s;
+  s.i0 = below ? 0 : (above ? n - 1 : k);
+  s.i1 = below ? 0 : (above ? n - 1 : k + 1);
+  s.hw0 = (below || above) ? 0.5 : 0.5 * (1.0 - t);
+  s.hw1 = (below || above) ? 0.0 : 0.5 * t;
+  return s;
 }
 
 // phase_mismatch (gn_integral.hpp:43-50), same grouping; -fmad=false keeps
@@ -89,16 +86,76 @@ __device__ __forceinline__ double phase_mismatch(double f1, double f2, double fi
 
 // Per-warp shared state for one chunk of 32 u2 columns.
 struct WarpSmem {
-  int col[6][32];    // stencil columns i0/i1 for nu1, nu2, nu3
+  int col[6][32];    // stencil columns i0/i1 for nu1, nu2, nu3 (times N: element offsets)
   double w[6][32];   // matching half weights
   double phi[32];
+  double invphi[32];  // 1/phi (0 when phi == 0: no fast span then)
   double pw[32];     // p1 * p2 * p3
   int src[32];       // chunk-local column of the listed point
   double val[32];    // pw * |kernel|^2 per chunk column
 };
 
+// Polynomial coefficients as __constant__ data: ptxas keeps them in uniform
+// registers (DFMA R, R, UR, R) instead of re-materialising 64-bit immediates
+// with UMOV/IMAD.MOV pairs every step, which cost v1 ~70 issue slots per step.
+__constant__ double c_e4[7] = {kE4c1, kE4c2, kE4c3, kE4c4, kE4c5, kE4c6, kE4c7};
+__constant__ double c_sin[6] = {kS1, kS2, kS3, kS4, kS5, kS6};
+__constant__ double c_cos[6] = {kC1, kC2, kC3, kC4, kC5, kC6};
+__constant__ double c_red[3] = {kTwoOverPi, -kPio2Hi, -kPio2Lo};
+
+// 2^(x/16), x = 16 log2 p (uwb_devmath.cuh exp2_16): 3 DADD + 7 DFMA + 1 DMUL,
+// one conflict-free LDS.
+__device__ __forceinline__ double dev_exp2_16(double x, const double* tab) {
+  const double t = x + kMagic;
+  const int k = __double2loint(t);
+  const double r = x - (t - kMagic);
+  double p = fma(r, c_e4[6], c_e4[5]);
+  p = fma(p, r, c_e4[4]);
+  p = fma(p, r, c_e4[3]);
+  p = fma(p, r, c_e4[2]);
+  p = fma(p, r, c_e4[1]);
+  p = fma(p, r, c_e4[0]);
+  p = fma(p, r, 1.0);
+  const double s = tab[k & 15] * p;
+  return __hiloint2double(__double2hiint(s) + ((k >> 4) << 20), __double2loint(s));
+}
+
+// (cos x, sin x) for |x| < 2^50 (uwb_devmath.cuh sincos_rd): 19 FP64 instructions.
+__device__ __forceinline__ void dev_sincos(double x, double* c_out, double* s_out) {
+  const double t = fma(x, c_red[0], kMagic);
+  const int q = __double2loint(t);
+  const double kd = t - kMagic;
+  double r = fma(kd, c_red[1], x);
+  r = fma(kd, c_red[2], r);
+  const double z = r * r;
+  double ps = fma(z, c_sin[5], c_sin[4]);
+  ps = fma(ps, z, c_sin[3]);
+  ps = fma(ps, z, c_sin[2]);
+  ps = fma(ps, z, c_sin[1]);
+  ps = fma(ps, z, c_sin[0]);
+  const double s = fma(r * z, ps, r);
+  double pc = fma(z, c_cos[5], c_cos[4]);
+  pc = fma(pc, z, c_cos[3]);
+  pc = fma(pc, z, c_cos[2]);
+  pc = fma(pc, z, c_cos[1]);
+  pc = fma(pc, z, c_cos[0]);
+  const double c = fma(z * z, pc, fma(z, -0.5, 1.0));
+  const bool swap = (q & 1) != 0;
+  const double so = swap ? c : s;
+  const double co = swap ? s : c;
+  *s_out = __hiloint2double(__double2hiint(so) ^ ((q & 2) << 30), __double2loint(so));
+  *c_out = __hiloint2double(__double2hiint(co) ^ (((q + 1) & 2) << 30), __double2loint(co));
+}
+
 // |sum over spans & steps|^2 for one point, computed by one 16-lane segment.
-template <int K>
+// Step m = sl + 16 b.  Fast branch (gn_integral.hpp:156-175) by summation by
+// parts: the lane of step m adds (p_m - p_{m+1}) E(z_{m+1}).  One rotating
+// shuffle per step serves every lane: lanes 0..14 receive p_{m+1} of the
+// same block; lane 15 receives lane 0's p of the current block, which is the
+// p_{m+1} of its own step from the previous block, whose term it deferred.
+// Slow branch (:176-188) is the direct sinc form.  Tables are padded past
+// the last step; lanes with m >= N mask p to 0 and feed sincos a 0 angle.
+template <int K, bool FULL>
 __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSmem& S, int idx,
                                                int probe, int sl, unsigned segmask,
                                                const double* tab) {
@@ -106,96 +163,107 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
   const double phi = S.phi[idx];
   const double w0 = S.w[0][idx], w1 = S.w[1][idx], w2 = S.w[2][idx];
   const double w3 = S.w[3][idx], w4 = S.w[4][idx], w5 = S.w[5][idx];
-  const size_t o0 = static_cast<size_t>(S.col[0][idx]) * N;
-  const size_t o1 = static_cast<size_t>(S.col[1][idx]) * N;
-  const size_t o2 = static_cast<size_t>(S.col[2][idx]) * N;
-  const size_t o3 = static_cast<size_t>(S.col[3][idx]) * N;
-  const size_t o4 = static_cast<size_t>(S.col[4][idx]) * N;
-  const size_t o5 = static_cast<size_t>(S.col[5][idx]) * N;
+  const int o0 = S.col[0][idx] + sl, o1 = S.col[1][idx] + sl, o2 = S.col[2][idx] + sl;
+  const int o3 = S.col[3][idx] + sl, o4 = S.col[4][idx] + sl, o5 = S.col[5][idx] + sl;
+  const int rot = (sl + 1) & 15;
   double fre = 0.0, fim = 0.0, sre = 0.0, sim = 0.0;
   for (int k = 0; k < P.n_spans; ++k) {
     const double* T = P.log2rho + k * P.span_stride;
-    const double* hl = P.hl2 + (static_cast<size_t>(probe) * P.n_spans + k) * N;
-    double p[K];
-#pragma unroll
-    for (int kk = 0; kk < K; ++kk) {
-      const int m = sl + 16 * kk;
-      p[kk] = 0.0;
-      if (m < N) {
-        double lg = fma(w0, __ldg(T + o0 + m), -__ldg(hl + m));
-        lg = fma(w1, __ldg(T + o1 + m), lg);
-        lg = fma(w2, __ldg(T + o2 + m), lg);
-        lg = fma(w3, __ldg(T + o3 + m), lg);
-        lg = fma(w4, __ldg(T + o4 + m), lg);
-        lg = fma(w5, __ldg(T + o5 + m), lg);
-        p[kk] = exp2_pos(lg, tab);
-      }
-    }
+    const double* c0 = T + o0;
+    const double* c1 = T + o1;
+    const double* c2 = T + o2;
+    const double* c3 = T + o3;
+    const double* c4 = T + o4;
+    const double* c5 = T + o5;
+    const double* hl = P.hl2 + (static_cast<size_t>(probe) * P.n_spans + k) * N + sl;
     const bool fast = fabs(phi) * __ldg(P.wlast + k) > 1e-4;
     if (fast) {
-      const double* ze = P.zedge + static_cast<size_t>(k) * (N + 1);
+      const double* ze = P.zedge + static_cast<size_t>(k) * (N + 1) + 1 + sl;
+      const bool l15 = sl == 15;
+      double pp = 0.0, pc = 0.0, ps = 0.0;  // previous block's (p, E): lane 15 defers
+      double pfirst = 0.0;
 #pragma unroll
-      for (int kk = 0; kk < K; ++kk) {
-        const int m = sl + 16 * kk;
-        // p_{m+1}: next lane, or lane 0 of the next step block for lane 15.
-        double pn = __shfl_down_sync(segmask, p[kk], 1, 16);
-        const double pw = (kk + 1 < K) ? __shfl_sync(segmask, p[kk + 1 < K ? kk + 1 : kk], 0, 16)
-                                       : 0.0;
-        if (sl == 15) pn = pw;
-        if (m < N) {
-          const double c = p[kk] - pn;
-          double cs, sn;
-          sincos_rd(phi * __ldg(ze + m + 1), &cs, &sn);
-          fre = fma(c, cs, fre);
-          fim = fma(c, sn, fim);
+      for (int b = 0; b < K; ++b) {
+        double lg = fma(w0, __ldg(c0 + 16 * b), -__ldg(hl + 16 * b));
+        lg = fma(w1, __ldg(c1 + 16 * b), lg);
+        lg = fma(w2, __ldg(c2 + 16 * b), lg);
+        lg = fma(w3, __ldg(c3 + 16 * b), lg);
+        lg = fma(w4, __ldg(c4 + 16 * b), lg);
+        lg = fma(w5, __ldg(c5 + 16 * b), lg);
+        double p = dev_exp2_16(lg, tab);
+        double ang = phi * __ldg(ze + 16 * b);
+        if (!FULL) {
+          const bool ok = sl + 16 * b < N;
+          p = ok ? p : 0.0;
+          ang = ok ? ang : 0.0;
         }
+        if (b == 0) pfirst = p;
+        double cs, sn;
+        dev_sincos(ang, &cs, &sn);
+        const double pr = __shfl_sync(segmask, p, rot, 16);
+        // lanes 0..14: (p_m - p_{m+1}) E_{m+1}; lane 15: the previous block's step
+        const double cc = (l15 ? pp : p) - pr;
+        fre = fma(cc, l15 ? pc : cs, fre);
+        fim = fma(cc, l15 ? ps : sn, fim);
+        pp = p;
+        pc = cs;
+        ps = sn;
       }
-      if (sl == 0) {
-        const double z0 = __ldg(ze);
-        double c0 = 1.0, s0 = 0.0;
-        if (z0 != 0.0) sincos_rd(phi * z0, &c0, &s0);
-        fre = fma(-p[0], c0, fre);
-        fim = fma(-p[0], s0, fim);
+      if (sl == 15) {  // p_N = 0
+        fre = fma(pp, pc, fre);
+        fim = fma(pp, ps, fim);
+      }
+      if (sl == 0) {  // -p_0 E(z_0)
+        const double z0 = __ldg(P.zedge + static_cast<size_t>(k) * (N + 1));
+        double c0v = 1.0, s0v = 0.0;
+        if (z0 != 0.0) dev_sincos(phi * z0, &c0v, &s0v);
+        fre = fma(-pfirst, c0v, fre);
+        fim = fma(-pfirst, s0v, fim);
       }
     } else {
-      const double* zm = P.zmid + static_cast<size_t>(k) * N;
-      const double* wd = P.width + static_cast<size_t>(k) * N;
-#pragma unroll
-      for (int kk = 0; kk < K; ++kk) {
-        const int m = sl + 16 * kk;
-        if (m < N) {
-          const double wm = __ldg(wd + m);
-          // sinc(x), |x| = |phi| w/2 <= 5e-5 on this branch: 1 - x^2/6 + x^4/120 is exact
+      const double* zm = P.zmid + static_cast<size_t>(k) * N + sl;
+      const double* wd = P.width + static_cast<size_t>(k) * N + sl;
+#pragma unroll 1
+      for (int b = 0; b < K; ++b) {
+        if (sl + 16 * b < N) {
+          double lg = fma(w0, __ldg(c0 + 16 * b), -__ldg(hl + 16 * b));
+          lg = fma(w1, __ldg(c1 + 16 * b), lg);
+          lg = fma(w2, __ldg(c2 + 16 * b), lg);
+          lg = fma(w3, __ldg(c3 + 16 * b), lg);
+          lg = fma(w4, __ldg(c4 + 16 * b), lg);
+          lg = fma(w5, __ldg(c5 + 16 * b), lg);
+          const double p = dev_exp2_16(lg, tab);
+          const double wm = __ldg(wd + 16 * b);
+          // sinc(x), |x| = |phi| w / 2 <= 5e-5 here: 1 - x^2/6 + x^4/120 is exact
           const double x = 0.5 * phi * wm;
           const double x2 = x * x;
           const double sinc = fma(x2, fma(x2, 1.0 / 120.0, -1.0 / 6.0), 1.0);
-          const double w = p[kk] * wm * sinc;
+          const double w = p * wm * sinc;
           double cs, sn;
-          sincos_rd(phi * __ldg(zm + m), &cs, &sn);
+          dev_sincos(phi * __ldg(zm + 16 * b), &cs, &sn);
           sre = fma(w, cs, sre);
           sim = fma(w, sn, sim);
         }
       }
     }
   }
+  // fast spans contribute (sum / (j phi)) (gn_integral.hpp:173-175)
+  const double invphi = S.invphi[idx];
+  double re = fma(fim, invphi, sre);
+  double im = fma(-fre, invphi, sim);
 #pragma unroll
   for (int o = 8; o >= 1; o >>= 1) {
-    fre += __shfl_xor_sync(segmask, fre, o, 16);
-    fim += __shfl_xor_sync(segmask, fim, o, 16);
-    sre += __shfl_xor_sync(segmask, sre, o, 16);
-    sim += __shfl_xor_sync(segmask, sim, o, 16);
+    re += __shfl_xor_sync(segmask, re, o, 16);
+    im += __shfl_xor_sync(segmask, im, o, 16);
   }
-  // fast spans contribute (sum / (j phi)) (gn_integral.hpp:173-175)
-  const double re = sre + fim / phi;
-  const double im = sim - fre / phi;
   return re * re + im * im;
 }
 
-template <int K>
+template <int K, bool FULL>
 __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParams P) {
-  __shared__ double s_tab[32];
+  __shared__ double s_tab[16];
   __shared__ WarpSmem s_w[kWarps];
-  if (threadIdx.x < 32) s_tab[threadIdx.x] = c_exp2_tab[threadIdx.x];
+  if (threadIdx.x < 16) s_tab[threadIdx.x] = c_exp2_tab16[threadIdx.x];
   __syncthreads();
 
   const int lane = threadIdx.x & 31;
@@ -205,6 +273,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
   const unsigned segmask = 0xffffu << (16 * seg);
   WarpSmem& S = s_w[warp];
   const int per_probe = P.n_q * P.n_r;
+  const int N = P.steps;
 
   for (;;) {
     int row = 0;
@@ -268,9 +337,10 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
         const double g2 = u1 / g1;
         const double f1 = s1 * g1;
         const double f2 = s2 * g2;
-        const double p1 = psd_and_stencil(P, nu + f1, &st1);
-        const double p2 = psd_and_stencil(P, nu + f2, &st2);
-        const double p3 = psd_and_stencil(P, nu + f1 + f2, &st3);
+        double p1, p2, p3;
+        st1 = psd_and_stencil(P, nu + f1, &p1);
+        st2 = psd_and_stencil(P, nu + f2, &p2);
+        st3 = psd_and_stencil(P, nu + f1 + f2, &p3);
         active = p1 != 0.0 && p2 != 0.0 && p3 != 0.0;
         if (active) {
           phi = phase_mismatch(f1, f2, f, P.beta2, P.beta3, P.beta4);
@@ -286,13 +356,14 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
       if (active) {
         // fast points first, then slow ones, so half-warp pairs rarely diverge
         const int pos = fast ? __popc(fm & lt) : __popc(fm) + __popc(sm & lt);
-        S.col[0][pos] = st1.i0; S.col[1][pos] = st1.i1;
-        S.col[2][pos] = st2.i0; S.col[3][pos] = st2.i1;
-        S.col[4][pos] = st3.i0; S.col[5][pos] = st3.i1;
-        S.w[0][pos] = st1.hw0; S.w[1][pos] = st1.hw1;
-        S.w[2][pos] = st2.hw0; S.w[3][pos] = st2.hw1;
-        S.w[4][pos] = st3.hw0; S.w[5][pos] = st3.hw1;
+        S.col[0][pos] = st1.i0 * N; S.col[1][pos] = st1.i1 * N;
+        S.col[2][pos] = st2.i0 * N; S.col[3][pos] = st2.i1 * N;
+        S.col[4][pos] = st3.i0 * N; S.col[5][pos] = st3.i1 * N;
+        S.w[0][pos] = st1.hw0 * 16.0; S.w[1][pos] = st1.hw1 * 16.0;
+        S.w[2][pos] = st2.hw0 * 16.0; S.w[3][pos] = st2.hw1 * 16.0;
+        S.w[4][pos] = st3.hw0 * 16.0; S.w[5][pos] = st3.hw1 * 16.0;
         S.phi[pos] = phi;
+        S.invphi[pos] = phi != 0.0 ? 1.0 / phi : 0.0;
         S.pw[pos] = pw;
         S.src[pos] = lane;
       }
@@ -300,7 +371,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
       const int n_act = __popc(am);
       n_eval += n_act;
       for (int idx = seg; idx < n_act; idx += 2) {
-        const double kv = point_kernel<K>(P, S, idx, probe, sl, segmask, s_tab);
+        const double kv = point_kernel<K, FULL>(P, S, idx, probe, sl, segmask, s_tab);
         if (sl == 0) S.val[S.src[idx]] = S.pw[idx] * kv;
       }
       __syncwarp();
@@ -322,14 +393,15 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
 __global__ void probe_halflog_kernel(const NliParams P) {
   const int probe = blockIdx.x;
   const double nu = P.probe_nu[probe];
-  Stencil sc;
-  psd_and_stencil(P, nu, &sc);
+  double unused;
+  const Stencil sc = psd_and_stencil(P, nu, &unused);
   for (int k = 0; k < P.n_spans; ++k) {
     const double* T = P.log2rho + k * P.span_stride;
     double* out = P.hl2 + (static_cast<size_t>(probe) * P.n_spans + k) * P.steps;
     for (int m = threadIdx.x; m < P.steps; m += blockDim.x) {
-      out[m] = sc.hw0 * T[static_cast<size_t>(sc.i0) * P.steps + m] +
-               sc.hw1 * T[static_cast<size_t>(sc.i1) * P.steps + m];
+      // 16 x (the reference's half-log, in log2): the integrand works in 2^-4 log2 units
+      out[m] = 16.0 * (sc.hw0 * T[static_cast<size_t>(sc.i0) * P.steps + m] +
+                        sc.hw1 * T[static_cast<size_t>(sc.i1) * P.steps + m]);
     }
   }
 }
@@ -382,29 +454,75 @@ __global__ void finalize_channels_kernel(const FinalizeParams F) {
 
 using RowKernel = void (*)(const NliParams);
 
+template <int K>
+RowKernel pick(int steps) {
+  return steps == 16 * K ? nli_rows_kernel<K, true> : nli_rows_kernel<K, false>;
+}
+
 RowKernel row_kernel_for(int steps) {
   switch ((steps + 15) / 16) {
-    case 1: return nli_rows_kernel<1>;
-    case 2: return nli_rows_kernel<2>;
-    case 3: return nli_rows_kernel<3>;
-    case 4: return nli_rows_kernel<4>;
-    case 5: return nli_rows_kernel<5>;
-    case 6: return nli_rows_kernel<6>;
-    case 7: return nli_rows_kernel<7>;
-    case 8: return nli_rows_kernel<8>;
-    case 9: return nli_rows_kernel<9>;
-    case 10: return nli_rows_kernel<10>;
-    case 11: return nli_rows_kernel<11>;
-    case 12: return nli_rows_kernel<12>;
-    case 13: return nli_rows_kernel<13>;
-    case 14: return nli_rows_kernel<14>;
-    case 15: return nli_rows_kernel<15>;
-    case 16: return nli_rows_kernel<16>;
+    case 1: return pick<1>(steps);
+    case 2: return pick<2>(steps);
+    case 3: return pick<3>(steps);
+    case 4: return pick<4>(steps);
+    case 5: return pick<5>(steps);
+    case 6: return pick<6>(steps);
+    case 7: return pick<7>(steps);
+    case 8: return pick<8>(steps);
+    case 9: return pick<9>(steps);
+    case 10: return pick<10>(steps);
+    case 11: return pick<11>(steps);
+    case 12: return pick<12>(steps);
+    case 13: return pick<13>(steps);
+    case 14: return pick<14>(steps);
+    case 15: return pick<15>(steps);
+    case 16: return pick<16>(steps);
     default: return nullptr;
   }
 }
 
+__global__ void __launch_bounds__(256) dfma_peak_kernel(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 }  // namespace
+
+double fp64_fma_peak_tflops(int sm_count, cudaStream_t st) {
+  const int blocks = sm_count * 8, threads = 256, iters = 2048;
+  double* out = nullptr;
+  if (cudaMalloc(&out, sizeof(double) * blocks * threads) != cudaSuccess) return 0.0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double best = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0, st);
+    dfma_peak_kernel<<<blocks, threads, 0, st>>>(out, iters, 0.9999999, 1e-7);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flops = 2.0 * 8 * 16 * static_cast<double>(iters) * blocks * threads;
+    if (rep > 0 && ms > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return best;
+}
 
 int launch_finalize_channels_only(const FinalizeParams& f, cudaStream_t st) {
   finalize_channels_kernel<<<(f.n_ch + 127) / 128, 128, 0, st>>>(f);

@@ -72,5 +72,12 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
 // CTAs per SM the integrand kernel reaches for a given step count.
 int nli_ctas_per_sm(int steps);
 constexpr int kMaxSteps = 256;  // 16 lanes x 16 steps per lane
+// Elements allocated past the end of log2rho / zedge / hl2: the integrand's
+// lanes with m >= N load them and mask the result (branch-free tail).
+constexpr int kTablePad = 32;
+
+// Live FP64 pipe peak (TFLOP/s): independent DFMA chains on every SM, timed
+// with CUDA events.  The roofline denominator for the integrand kernel.
+double fp64_fma_peak_tflops(int sm_count, cudaStream_t stream);  // 16 lanes x 16 steps per lane
 
 }  // namespace uwb

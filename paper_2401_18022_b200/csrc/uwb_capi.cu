@@ -87,21 +87,21 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   }
   double* d_freq = c->freq.get<double>(n);
   double* d_psd = c->psd.get<double>(n);
-  double* d_tab = c->log2rho.get<double>(tab.size());
-  double* d_ze = c->zedge.get<double>(ze.size());
+  double* d_tab = c->log2rho.get<double>(tab.size() + kTablePad);  // lanes past N read the pad
+  double* d_ze = c->zedge.get<double>(ze.size() + kTablePad);
   double* d_zm = c->zmid.get<double>(zm.size());
   double* d_wd = c->width.get<double>(wd.size());
   double* d_wl = c->wlast.get<double>(wl.size());
   if (!d_freq || !d_psd || !d_tab || !d_ze || !d_zm || !d_wd || !d_wl)
     return fail(UWB_CUDA_ERROR, "device allocation failed");
   cudaStream_t st = c->stream;
-  cudaMemcpyAsync(d_freq, g->freq, n * sizeof(double), cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(d_psd, g->psd, n * sizeof(double), cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(d_ze, ze.data(), ze.size() * sizeof(double), cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(d_zm, zm.data(), zm.size() * sizeof(double), cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(d_wd, wd.data(), wd.size() * sizeof(double), cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(d_wl, wl.data(), wl.size() * sizeof(double), cudaMemcpyHostToDevice, st);
+  xfer(c, d_freq, g->freq, n * sizeof(double), cudaMemcpyHostToDevice, st);
+  xfer(c, d_psd, g->psd, n * sizeof(double), cudaMemcpyHostToDevice, st);
+  xfer(c, d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st);
+  xfer(c, d_ze, ze.data(), ze.size() * sizeof(double), cudaMemcpyHostToDevice, st);
+  xfer(c, d_zm, zm.data(), zm.size() * sizeof(double), cudaMemcpyHostToDevice, st);
+  xfer(c, d_wd, wd.data(), wd.size() * sizeof(double), cudaMemcpyHostToDevice, st);
+  xfer(c, d_wl, wl.data(), wl.size() * sizeof(double), cudaMemcpyHostToDevice, st);
   // the vectors die at return: make the copies complete first
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "upload");
@@ -124,6 +124,8 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   P->beta2 = beta[0];
   P->beta3 = beta[1];
   P->beta4 = beta[2];
+  c->last_steps = steps;
+  c->last_spans = n_spans;
   return UWB_OK;
 }
 
@@ -162,7 +164,7 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
   P.n_probes = np;
   P.total_rows = np * P.n_q * P.n_r;
   P.probe_nu = d_nu;
-  P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * P.steps);
+  P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * P.steps + kTablePad);
   P.rowsum = c->rowsum.get<double>(std::max(P.total_rows, 1));
   P.counter = c->counter.get<unsigned int>(1);
   P.n_eval = c->n_eval.get<unsigned long long>(1);
@@ -173,8 +175,8 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
     return fail(UWB_CUDA_ERROR, "device allocation failed");
   cudaStream_t st = c->stream;
   if (np) {
-    cudaMemcpyAsync(d_nu, nu.data(), np * sizeof(double), cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(d_g, gam.data(), np * sizeof(double), cudaMemcpyHostToDevice, st);
+    xfer(c, d_nu, nu.data(), np * sizeof(double), cudaMemcpyHostToDevice, st);
+    xfer(c, d_g, gam.data(), np * sizeof(double), cudaMemcpyHostToDevice, st);
   }
   if (chan_probe0) {
     const int n = P.n_ch;
@@ -189,7 +191,7 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
     F.nli_power = c->nli_power.get<double>(n);
     F.quad = c->quad.get<double>(4 * n);
     F.skipped = c->skipped.get<uint8_t>(n);
-    cudaMemcpyAsync(d_cp, chan_probe0->data(), n * sizeof(int), cudaMemcpyHostToDevice, st);
+    xfer(c, d_cp, chan_probe0->data(), n * sizeof(int), cudaMemcpyHostToDevice, st);
   }
   cudaEventRecord(c->ev0, st);
   if (np) {
@@ -198,6 +200,7 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
     const int launched = launch_nli(P, F, c->sm_count * per_sm, st, c->evk0, c->evk1);
     if (launched < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
     c->last_launches = launched;
+    c->nli_events_valid = true;
   } else {
     // every channel skipped: only the channel epilogue
     c->last_launches = launch_finalize_channels_only(F, st);
@@ -213,7 +216,7 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
       cudaEventElapsedTime(&ms, c->evk0, c->evk1);
       c->last_kernel_ms = ms;
       unsigned long long ne = 0;
-      cudaMemcpy(&ne, P.n_eval, sizeof ne, cudaMemcpyDeviceToHost);
+      xfer_sync(c, &ne, P.n_eval, sizeof ne, cudaMemcpyDeviceToHost);
       c->last_points = static_cast<double>(ne);
       c->last_inner_steps = static_cast<double>(ne) * P.steps * P.n_spans;
     }
@@ -331,6 +334,7 @@ int uwb_all_channels_nli(uwb_ctx* c, const uwb_grid* grid, int n_spans, const uw
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
   cudaSetDevice(c->device);
   release_link_state(c);  // shares buffers with the prepared evaluation
+  reset_xfer(c);
   int rc = validate_grid(grid);
   if (rc) return rc;
   NliParams P{};
@@ -347,22 +351,22 @@ int uwb_all_channels_nli(uwb_ctx* c, const uwb_grid* grid, int n_spans, const uw
     P.n_ch = n;
     P.psd = c->psd.get<double>(n);
     P.bch = grid->bch;
-    cudaMemcpyAsync(const_cast<double*>(P.psd), grid->psd, n * sizeof(double),
+    xfer(c, const_cast<double*>(P.psd), grid->psd, n * sizeof(double),
                     cudaMemcpyHostToDevice, c->stream);
   }
   if ((rc = run_probes(c, P, cfg, nu, gam, &cp, true))) return rc;
   const int n = grid->n_ch;
   cudaStream_t st = c->stream;
   if (out) {
-    if (out->eta) cudaMemcpyAsync(out->eta, c->eta.ptr<double>(), n * 8, cudaMemcpyDeviceToHost, st);
+    if (out->eta) xfer(c, out->eta, c->eta.ptr<double>(), n * 8, cudaMemcpyDeviceToHost, st);
     if (out->nli_psd)
-      cudaMemcpyAsync(out->nli_psd, c->nli_psd.ptr<double>(), n * 8, cudaMemcpyDeviceToHost, st);
+      xfer(c, out->nli_psd, c->nli_psd.ptr<double>(), n * 8, cudaMemcpyDeviceToHost, st);
     if (out->nli_power)
-      cudaMemcpyAsync(out->nli_power, c->nli_power.ptr<double>(), n * 8, cudaMemcpyDeviceToHost, st);
+      xfer(c, out->nli_power, c->nli_power.ptr<double>(), n * 8, cudaMemcpyDeviceToHost, st);
     if (out->quadrant)
-      cudaMemcpyAsync(out->quadrant, c->quad.ptr<double>(), n * 32, cudaMemcpyDeviceToHost, st);
+      xfer(c, out->quadrant, c->quad.ptr<double>(), n * 32, cudaMemcpyDeviceToHost, st);
     if (out->skipped)
-      cudaMemcpyAsync(out->skipped, c->skipped.ptr<uint8_t>(), n, cudaMemcpyDeviceToHost, st);
+      xfer(c, out->skipped, c->skipped.ptr<uint8_t>(), n, cudaMemcpyDeviceToHost, st);
   }
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "all_channels_nli");
@@ -380,6 +384,7 @@ int uwb_nli_psd_at(uwb_ctx* c, const uwb_grid* grid, int n_spans, const uwb_span
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
   cudaSetDevice(c->device);
   release_link_state(c);
+  reset_xfer(c);
   int rc = validate_grid(grid);
   if (rc) return rc;
   NliParams P{};
@@ -389,9 +394,9 @@ int uwb_nli_psd_at(uwb_ctx* c, const uwb_grid* grid, int n_spans, const uwb_span
   std::vector<double> vnu(nu, nu + n_probe), vg(gamma, gamma + n_probe);
   if ((rc = run_probes(c, P, cfg, vnu, vg, nullptr, true))) return rc;
   cudaStream_t st = c->stream;
-  if (out) cudaMemcpyAsync(out, c->probe_g.ptr<double>(), n_probe * 8, cudaMemcpyDeviceToHost, st);
+  if (out) xfer(c, out, c->probe_g.ptr<double>(), n_probe * 8, cudaMemcpyDeviceToHost, st);
   if (quadrant4)
-    cudaMemcpyAsync(quadrant4, c->probe_quad.ptr<double>(), n_probe * 32, cudaMemcpyDeviceToHost, st);
+    xfer(c, quadrant4, c->probe_quad.ptr<double>(), n_probe * 32, cudaMemcpyDeviceToHost, st);
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "nli_psd_at");
   return UWB_OK;
@@ -423,9 +428,38 @@ int uwb_last_launch_count(uwb_ctx* c) { return c ? c->last_launches : 0; }
 int uwb_last_nli_stats(uwb_ctx* c, double* kernel_ms, double* inner_steps,
                        double* evaluated_points) {
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  // Resolved lazily from the events/counter of the last integrand launch (the
+  // caller has synchronised), so the resident path pays nothing per call.
+  if (c->nli_events_valid) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(c->evk1) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, c->evk0, c->evk1) == cudaSuccess)
+      c->last_kernel_ms = ms;
+    const unsigned long long* d_ne = c->n_eval.ptr<unsigned long long>();
+    unsigned long long ne = 0;
+    if (d_ne) cudaMemcpy(&ne, d_ne, sizeof ne, cudaMemcpyDeviceToHost);
+    c->last_points = static_cast<double>(ne);
+    c->last_inner_steps = static_cast<double>(ne) * c->last_steps * c->last_spans;
+  }
   if (kernel_ms) *kernel_ms = c->last_kernel_ms;
   if (inner_steps) *inner_steps = c->last_inner_steps;
   if (evaluated_points) *evaluated_points = c->last_points;
+  return UWB_OK;
+}
+
+int uwb_last_transfer_bytes(uwb_ctx* c, unsigned long long* h2d, unsigned long long* d2h) {
+  if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  if (h2d) *h2d = c->h2d_bytes;
+  if (d2h) *d2h = c->d2h_bytes;
+  return UWB_OK;
+}
+
+int uwb_fp64_peak(uwb_ctx* c, double* tflops) {
+  if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  cudaSetDevice(c->device);
+  const double t = fp64_fma_peak_tflops(c->sm_count, c->stream);
+  if (!(t > 0)) return set_err(UWB_CUDA_ERROR, "fp64 microbenchmark failed");
+  if (tflops) *tflops = t;
   return UWB_OK;
 }
 

@@ -13,6 +13,22 @@
 namespace uwb {
 
 int fail(int code, const std::string& msg);
+
+// cudaMemcpy(Async) that accounts host<->device bytes on the context
+// (uwb_last_transfer_bytes: the e2e bench reports them per step).
+inline cudaError_t xfer(uwb_ctx* c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                        cudaStream_t st) {
+  if (kind == cudaMemcpyHostToDevice) c->h2d_bytes += bytes;
+  if (kind == cudaMemcpyDeviceToHost) c->d2h_bytes += bytes;
+  return cudaMemcpyAsync(dst, src, bytes, kind, st);
+}
+inline cudaError_t xfer_sync(uwb_ctx* c, void* dst, const void* src, size_t bytes,
+                             cudaMemcpyKind kind) {
+  cudaError_t e = xfer(c, dst, src, bytes, kind, c->stream);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(c->stream);
+}
+inline void reset_xfer(uwb_ctx* c) { c->h2d_bytes = c->d2h_bytes = 0; }
 int cuda_fail(cudaError_t e, const char* what);
 int validate_grid(const uwb_grid* g);
 int set_cfg(const uwb_nli_cfg* cfg, NliParams* P);

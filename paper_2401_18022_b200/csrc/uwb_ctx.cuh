@@ -64,7 +64,10 @@ struct uwb_ctx {
   uwb::DBuf alpha, aeff, raman_x, raman_y, nf_db, guard, rho_end, ode_work, report, mid, edge;
   std::vector<int> subset;
   // stats of the last call
+  unsigned long long h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of the last call
   int last_launches = 0;
+  bool nli_events_valid = false;
+  int last_steps = 0, last_spans = 1;  // of the last non-resident NLI upload  // evk0/evk1 bracket the last integrand launch
   double last_kernel_ms = 0.0;
   double last_inner_steps = 0.0;
   double last_points = 0.0;

@@ -82,6 +82,43 @@ UWB_HD double fmad(double a, double b, double c) {
    1.681792830507429, 1.718619298122478, 1.7562521603732995, 1.7947090750031072,  \
    1.8340080864093424, 1.8741676341103, 1.9152065613971474, 1.9571441241754002}
 
+// 2^(j/128), j = 0..127, correctly rounded (60-digit arithmetic).
+#define UWB_EXP2_TABLE128 \
+  { \
+    1.0, 1.0054299011128027, 1.0108892860517005, 1.016378314910953, \
+    1.0218971486541166, 1.0274459491187637, 1.0330248790212284, 1.0386341019613787, \
+    1.0442737824274138, 1.0499440858006872, 1.0556451783605572, 1.061377227289262, \
+    1.0671404006768237, 1.0729348675259756, 1.0787607977571199, 1.0846183622133092, \
+    1.0905077326652577, 1.0964290818163769, 1.102382583307841, 1.1083684117236787, \
+    1.1143867425958924, 1.1204377524096067, 1.1265216186082418, 1.1326385195987192, \
+    1.1387886347566916, 1.1449721444318042, 1.1511892299529827, 1.1574400736337511, \
+    1.1637248587775775, 1.1700437696832502, 1.1763969916502812, 1.182784710984341, \
+    1.189207115002721, 1.1956643920398273, 1.202156731452703, 1.2086843236265816, \
+    1.215247359980469, 1.2218460329727576, 1.22848053610687, 1.2351510639369334, \
+    1.241857812073484, 1.2486009771892048, 1.255380757024691, 1.2621973503942507, \
+    1.2690509571917332, 1.275941778396392, 1.2828700160787783, 1.2898358734066657, \
+    1.2968395546510096, 1.3038812651919358, 1.3109612115247644, 1.318079601266064, \
+    1.3252366431597413, 1.3324325470831615, 1.339667524053303, 1.3469417862329458, \
+    1.3542555469368927, 1.3616090206382248, 1.3690024229745905, 1.3764359707545302, \
+    1.383909881963832, 1.3914243757719262, 1.3989796725383112, 1.4065759938190154, \
+    1.4142135623730951, 1.4218926021691656, 1.42961333839197, 1.4373759974489824, \
+    1.4451808069770467, 1.4530279958490526, 1.460917794180647, 1.4688504333369818, \
+    1.4768261459394993, 1.4848451658727524, 1.4929077282912648, 1.5010140696264256, \
+    1.5091644275934228, 1.5173590411982147, 1.5255981507445384, 1.533881997840956, \
+    1.5422108254079407, 1.550584877685, 1.559004400237837, 1.567469639965553, \
+    1.5759808451078865, 1.5845382652524937, 1.593142151342267, 1.6017927556826934, \
+    1.6104903319492543, 1.6192351351948637, 1.6280274218573478, 1.6368674497669644, \
+    1.645755478153965, 1.6546917676561943, 1.6636765803267364, 1.6727101796415966, \
+    1.681792830507429, 1.6909247992693053, 1.7001063537185235, 1.709337763100463, \
+    1.718619298122478, 1.7279512309618377, 1.7373338352737062, 1.746767386199169, \
+    1.7562521603732995, 1.7657884359332727, 1.7753764925265212, 1.785016611318935, \
+    1.7947090750031072, 1.804454167806624, 1.8142521755003989, 1.8241033854070534, \
+    1.8340080864093424, 1.843966568958626, 1.8539791250833855, 1.864046048397789, \
+    1.8741676341103, 1.8843441790323345, 1.8945759815869656, 1.9048633418176741, \
+    1.9152065613971474, 1.925605943636125, 1.9360617934922943, 1.9465744175792332, \
+    1.9571441241754002, 1.9677712232331759, 1.978456026387951, 1.9891988469672663 \
+  }
+
 // Taylor coefficients of 2^r = exp(r ln2): (ln 2)^n / n!
 constexpr double kE2c1 = 0.69314718055994530942;
 constexpr double kE2c2 = 0.24022650695910071233;
@@ -105,6 +142,60 @@ UWB_HD double exp2_pos(double x, const double* tab) {
   p = fmad(p, r, 1.0);
   const double s = tab[k & 31] * p;
   return from_words(hi_word(s) + ((k >> 5) << 20), lo_word(s));
+}
+
+// 2^(x/128) for the integrand's tables pre-scaled by 128 (x = 128 log2 p):
+// k = rint(x) by DADD, r = x - k exact in [-1/2, 1/2], 2^(r/128) by a degree-5
+// Taylor polynomial (|r ln2/128| <= 0.0027: truncation 5.4e-19), table 2^(j/128).
+constexpr double kE7c1 = 0.0054152123481245725;
+constexpr double kE7c2 = 1.4662262387640425e-05;
+constexpr double kE7c3 = 2.646642144433097e-08;
+constexpr double kE7c4 = 3.583032305400251e-11;
+constexpr double kE7c5 = 3.880576156786539e-14;
+
+UWB_HD double exp2_128(double x, const double* tab128) {
+  const double t = x + kMagic;
+  const int k = lo_word(t);
+  const double r = x - (t - kMagic);
+  double p = fmad(kE7c5, r, kE7c4);
+  p = fmad(p, r, kE7c3);
+  p = fmad(p, r, kE7c2);
+  p = fmad(p, r, kE7c1);
+  p = fmad(p, r, 1.0);
+  const double s = tab128[k & 127] * p;
+  return from_words(hi_word(s) + ((k >> 7) << 20), lo_word(s));
+}
+
+// 2^(x/16) for the integrand's tables pre-scaled by 16 (x = 16 log2 p): k =
+// rint(x) by DADD, r = x - k exact in [-1/2, 1/2], 2^(r/16) by a degree-7
+// Taylor polynomial (|r ln2/16| <= 0.0217: truncation 1.2e-18), table 2^(j/16).
+// 16 doubles fill the 32 shared-memory banks exactly: lookups never conflict.
+#define UWB_EXP2_TABLE16                                                                    \
+  {1.0, 1.0442737824274138, 1.0905077326652577, 1.1387886347566916, 1.189207115002721,      \
+   1.241857812073484, 1.2968395546510096, 1.3542555469368927, 1.4142135623730951,           \
+   1.4768261459394993, 1.5422108254079407, 1.6104903319492543, 1.681792830507429,           \
+   1.7562521603732995, 1.8340080864093424, 1.9152065613971474}
+constexpr double kE4c1 = 0.04332169878499658;
+constexpr double kE4c2 = 0.0009383847928089872;
+constexpr double kE4c3 = 1.3550807779497457e-05;
+constexpr double kE4c4 = 1.467610032291943e-07;
+constexpr double kE4c5 = 1.2715871950558131e-09;
+constexpr double kE4c6 = 9.181219573844438e-12;
+constexpr double kE4c7 = 5.682086126528621e-14;
+
+UWB_HD double exp2_16(double x, const double* tab16) {
+  const double t = x + kMagic;
+  const int k = lo_word(t);
+  const double r = x - (t - kMagic);
+  double p = fmad(kE4c7, r, kE4c6);
+  p = fmad(p, r, kE4c5);
+  p = fmad(p, r, kE4c4);
+  p = fmad(p, r, kE4c3);
+  p = fmad(p, r, kE4c2);
+  p = fmad(p, r, kE4c1);
+  p = fmad(p, r, 1.0);
+  const double s = tab16[k & 15] * p;
+  return from_words(hi_word(s) + ((k >> 4) << 20), lo_word(s));
 }
 
 // pi/2 split for the reduction: kPio2Hi = RN(pi/2), kPio2Lo = RN(pi/2 - kPio2Hi).

@@ -146,7 +146,7 @@ namespace {
 template <class T>
 T* up(uwb_ctx* c, DBuf& b, const T* src, size_t n) {
   T* d = b.get<T>(std::max<size_t>(n, 1));
-  if (d && src && n) cudaMemcpyAsync(d, src, n * sizeof(T), cudaMemcpyHostToDevice, c->stream);
+  if (d && src && n) xfer(c, d, src, n * sizeof(T), cudaMemcpyHostToDevice, c->stream);
   return d;
 }
 
@@ -256,8 +256,9 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   P.half_band = g->half_band;
   P.n_spans = fb->span_count;
   P.steps = steps;
-  P.log2rho = c->log2rho.get<double>(static_cast<size_t>(n) * steps);
+  P.log2rho = c->log2rho.get<double>(static_cast<size_t>(n) * steps + kTablePad);
   P.span_stride = 0;
+  ze.resize(ze.size() + kTablePad, 0.0);  // lanes past N read the pad
   P.zedge = up(c, c->zedge, ze.data(), ze.size());
   P.zmid = up(c, c->zmid, zm.data(), zm.size());
   P.width = up(c, c->width, wd.data(), wd.size());
@@ -265,6 +266,8 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   P.beta2 = fb->beta[0];
   P.beta3 = fb->beta[1];
   P.beta4 = fb->beta[2];
+  c->last_steps = steps;
+  c->last_spans = fb->span_count;
 
   // probes: channels with launch power (the resident path keeps this set)
   std::vector<double> nu, gam;
@@ -277,7 +280,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   P.n_probes = np;
   P.total_rows = np * P.n_q * P.n_r;
   P.probe_nu = up(c, c->probe_nu, nu.data(), nu.size());
-  P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * steps);
+  P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * steps + kTablePad);
   P.rowsum = c->rowsum.get<double>(std::max(P.total_rows, 1));
   P.counter = c->counter.get<unsigned int>(1);
   P.n_eval = c->n_eval.get<unsigned long long>(1);
@@ -328,7 +331,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   O.rho_end = d_rho_end;
   O.status = pr->d_status;
   O.rhs_evals = pr->d_rhs;
-  cudaMemcpyAsync(d_band2, band.data(), n * sizeof(int), cudaMemcpyHostToDevice, c->stream);
+  xfer(c, d_band2, band.data(), n * sizeof(int), cudaMemcpyHostToDevice, c->stream);
 
   // assembly
   LinkDev& L = pr->L;
@@ -356,12 +359,14 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   return UWB_OK;
 }
 
-// One evaluation on the prepared state; psd_dev = launch PSD (device).
-int run_prepared(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool stats) {
+// Noise stage of one evaluation on the prepared state (solve_link_noise,
+// link_optimizer.hpp:181-190): Raman ODE + NLI for the context's channels.
+// psd_dev = launch PSD (device) or null to keep the prepared one.
+int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st) {
   uwb_ctx::Prepared* pr = c->prep;
   int launches = 0;
   if (psd_dev && psd_dev != pr->d_psd)
-    cudaMemcpyAsync(pr->d_psd, psd_dev, pr->n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    xfer(c, pr->d_psd, psd_dev, pr->n * sizeof(double), cudaMemcpyDeviceToDevice, st);
   cudaMemsetAsync(pr->d_status, 0, sizeof(int), st);
   cudaEventRecord(c->ev0, st);
   const int lo = launch_raman_ode(pr->O, pr->P.freq, pr->d_psd, pr->P.bch, pr->d_aeff, pr->d_rx,
@@ -370,27 +375,44 @@ int run_prepared(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool stats)
   if (lo < 0) return fail(UWB_CUDA_ERROR, "raman ODE launch failed (cluster/smem)");
   launches += lo;
   if (pr->P.n_probes > 0) {
-    const int ln = launch_nli(pr->P, pr->F, pr->grid_ctas, st, stats ? c->evk0 : nullptr,
-                              stats ? c->evk1 : nullptr);
+    const int ln = launch_nli(pr->P, pr->F, pr->grid_ctas, st, c->evk0, c->evk1);
     if (ln < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
     launches += ln;
+    c->nli_events_valid = true;
   } else {
     launches += launch_finalize_channels_only(pr->F, st);
+    c->nli_events_valid = false;
   }
-  LinkDev L = pr->L;
-  link_channels_kernel<<<(L.n + 127) / 128, 128, 0, st>>>(L);
-  link_totals_kernel<<<1, 32, 0, st>>>(L);
-  launches += 2;
-  cudaEventRecord(c->ev1, st);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "evaluate_link launch");
   c->last_launches = launches;
   return UWB_OK;
 }
 
+// Report stage (assemble_link_report, link_optimizer.hpp:194-237).
+int run_report(uwb_ctx* c, cudaStream_t st) {
+  LinkDev L = c->prep->L;
+  link_channels_kernel<<<(L.n + 127) / 128, 128, 0, st>>>(L);
+  link_totals_kernel<<<1, 32, 0, st>>>(L);
+  c->last_launches += 2;
+  cudaEventRecord(c->ev1, st);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "assemble_link_report launch");
+  return UWB_OK;
+}
+
+int run_prepared(uwb_ctx* c, const double* psd_dev, cudaStream_t st) {
+  int rc = run_noise(c, psd_dev, st);
+  if (rc) return rc;
+  const int l = c->last_launches;
+  rc = run_report(c, st);
+  c->last_launches = l + 2;
+  return rc;
+}
+
 int check_status(uwb_ctx* c) {
   int status = 0;
-  cudaMemcpy(&status, c->prep->d_status, sizeof(int), cudaMemcpyDeviceToHost);
+  xfer_sync(c, &status, c->prep->d_status, sizeof(int), cudaMemcpyDeviceToHost);
   switch (status) {
     case 0: return UWB_OK;
     case 1: return fail(UWB_SOLVER_ERROR, "power evolution: non-positive rho");
@@ -417,11 +439,12 @@ int uwb_evaluate_link_resident(uwb_ctx* c, const double* psd_dev, double* report
                                void* stream) {
   if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
-  int rc = run_prepared(c, psd_dev, st, false);
+  reset_xfer(c);
+  int rc = run_prepared(c, psd_dev, st);
   if (rc) return rc;
   if (report_dev) {
     const size_t cnt = 4 * static_cast<size_t>(c->prep->n) + 3 + 2 * c->prep->L.n_bands;
-    cudaMemcpyAsync(report_dev, c->prep->L.out, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    xfer(c, report_dev, c->prep->L.out, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st);
   }
   return UWB_OK;
 }
@@ -430,16 +453,17 @@ int uwb_evaluate_link(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
                       const uwb_link_cfg* link, const uwb_nli_cfg* cfg, uwb_link_report* out) {
   if (!c) return fail(UWB_CONFIG_ERROR, "null context");
   cudaSetDevice(c->device);
+  reset_xfer(c);
   int rc = prepare(c, grid, fibre, link, cfg);
   if (rc) return rc;
   uwb_ctx::Prepared* pr = c->prep;
-  if ((rc = run_prepared(c, nullptr, c->stream, true))) return rc;
+  if ((rc = run_prepared(c, nullptr, c->stream))) return rc;
   const int n = pr->n;
   cudaStream_t st = c->stream;
   std::vector<double> rep(4 * static_cast<size_t>(n) + 3 + 2 * pr->L.n_bands);
-  cudaMemcpyAsync(rep.data(), pr->L.out, rep.size() * sizeof(double), cudaMemcpyDeviceToHost, st);
+  xfer(c, rep.data(), pr->L.out, rep.size() * sizeof(double), cudaMemcpyDeviceToHost, st);
   if (out && out->rho_end)
-    cudaMemcpyAsync(out->rho_end, pr->O.rho_end, n * sizeof(double), cudaMemcpyDeviceToHost, st);
+    xfer(c, out->rho_end, pr->O.rho_end, n * sizeof(double), cudaMemcpyDeviceToHost, st);
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "evaluate_link");
   if ((rc = check_status(c))) return rc;
@@ -466,11 +490,42 @@ int uwb_evaluate_link(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
     cudaEventElapsedTime(&kms, c->evk0, c->evk1);
     c->last_kernel_ms = kms;
     unsigned long long ne = 0;
-    cudaMemcpy(&ne, pr->P.n_eval, sizeof ne, cudaMemcpyDeviceToHost);
+    xfer_sync(c, &ne, pr->P.n_eval, sizeof ne, cudaMemcpyDeviceToHost);
     c->last_points = static_cast<double>(ne);
     c->last_inner_steps = static_cast<double>(ne) * pr->P.steps * pr->P.n_spans;
   }
   return UWB_OK;
+}
+
+int uwb_evaluate_link_resident_noise(uwb_ctx* c, const double* psd_dev, void* stream) {
+  if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
+  reset_xfer(c);
+  return run_noise(c, psd_dev, stream ? static_cast<cudaStream_t>(stream) : c->stream);
+}
+
+int uwb_evaluate_link_resident_report(uwb_ctx* c, double* report_dev, void* stream) {
+  if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+  c->last_launches = 0;
+  int rc = run_report(c, st);
+  if (rc) return rc;
+  if (report_dev) {
+    const size_t cnt = 4 * static_cast<size_t>(c->prep->n) + 3 + 2 * c->prep->L.n_bands;
+    xfer(c, report_dev, c->prep->L.out, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  }
+  return UWB_OK;
+}
+
+int uwb_link_eta_buffer(uwb_ctx* c, double** eta_dev, int* n_ch) {
+  if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
+  if (eta_dev) *eta_dev = c->prep->F.eta;
+  if (n_ch) *n_ch = c->prep->n;
+  return UWB_OK;
+}
+
+int uwb_resident_status(uwb_ctx* c) {
+  if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
+  return check_status(c);
 }
 
 int uwb_power_evolution(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
@@ -479,6 +534,7 @@ int uwb_power_evolution(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre
   if (!c) return fail(UWB_CONFIG_ERROR, "null context");
   cudaSetDevice(c->device);
   release_link_state(c);  // shares buffers with the prepared evaluation
+  reset_xfer(c);
   int rc = validate_grid(grid);
   if (rc) return rc;
   if (!fibre || !link || !fibre->alpha || !fibre->aeff)
@@ -525,10 +581,10 @@ int uwb_power_evolution(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre
                                   fibre->raman_aeff_ref, w, d_lo, d_lo + n, st);
   if (lo < 0) return fail(UWB_CUDA_ERROR, "raman ODE launch failed (cluster/smem)");
   c->last_launches = lo;
-  if (log_rho) cudaMemcpyAsync(log_rho, d_ln, static_cast<size_t>(n) * steps * 8, cudaMemcpyDeviceToHost, st);
-  if (rho_end) cudaMemcpyAsync(rho_end, d_re, n * 8, cudaMemcpyDeviceToHost, st);
+  if (log_rho) xfer(c, log_rho, d_ln, static_cast<size_t>(n) * steps * 8, cudaMemcpyDeviceToHost, st);
+  if (rho_end) xfer(c, rho_end, d_re, n * 8, cudaMemcpyDeviceToHost, st);
   int status = 0;
-  cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st);
+  xfer(c, &status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st);
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "power evolution");
   if (status == 1) return fail(UWB_SOLVER_ERROR, "power evolution: non-positive rho");

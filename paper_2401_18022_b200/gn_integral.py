@@ -283,6 +283,16 @@ class Engine:
     def last_launches(self):
         return self.lib.uwb_last_launch_count(self.h)
 
+    def last_transfer_bytes(self):
+        a, b = N.C.c_ulonglong(), N.C.c_ulonglong()
+        N.check(self.lib.uwb_last_transfer_bytes(self.h, N.C.byref(a), N.C.byref(b)))
+        return a.value, b.value
+
+    def fp64_peak_tflops(self):
+        t = N.C.c_double()
+        N.check(self.lib.uwb_fp64_peak(self.h, N.C.byref(t)))
+        return t.value
+
     def last_nli_stats(self):
         a, b, c = N.C.c_double(), N.C.c_double(), N.C.c_double()
         N.check(self.lib.uwb_last_nli_stats(self.h, N.C.byref(a), N.C.byref(b), N.C.byref(c)))
@@ -504,6 +514,24 @@ class ResidentLink:
         self.report_len = 4 * self.n + 3 + 2 * N_BANDS
 
     def run(self, psd_dev_ptr: int, report_dev_ptr: int, stream_ptr: int = 0):
+        """ODE + NLI + SNR assembly for the launch PSD at psd_dev_ptr."""
         N.check(self.eng.lib.uwb_evaluate_link_resident(self.eng.h, N.C.c_void_p(psd_dev_ptr),
                                                         N.C.c_void_p(report_dev_ptr),
                                                         N.C.c_void_p(stream_ptr)))
+
+    # split form for multi-GPU: noise on this rank's channels, all-reduce eta, report
+    def run_noise(self, psd_dev_ptr: int, stream_ptr: int = 0):
+        N.check(self.eng.lib.uwb_evaluate_link_resident_noise(
+            self.eng.h, N.C.c_void_p(psd_dev_ptr), N.C.c_void_p(stream_ptr)))
+
+    def run_report(self, report_dev_ptr: int, stream_ptr: int = 0):
+        N.check(self.eng.lib.uwb_evaluate_link_resident_report(
+            self.eng.h, N.C.c_void_p(report_dev_ptr), N.C.c_void_p(stream_ptr)))
+
+    def eta_buffer(self):
+        p, n = N.C.c_void_p(), N.C.c_int()
+        N.check(self.eng.lib.uwb_link_eta_buffer(self.eng.h, N.C.byref(p), N.C.byref(n)))
+        return p.value, n.value
+
+    def check_status(self):
+        N.check(self.eng.lib.uwb_resident_status(self.eng.h))
