@@ -84,15 +84,18 @@ __device__ __forceinline__ double phase_mismatch(double f1, double f2, double fi
   return -4.0 * kPi * kPi * (f1 * f2) * bracket;
 }
 
-// Per-warp shared state for one chunk of 32 u2 columns.
+// Per-warp shared state for one chunk of 32 u2 columns, plus the row's
+// parameters (parked here so they are not live in registers across the
+// integrand loop).
 struct WarpSmem {
-  int col[6][32];    // stencil columns i0/i1 for nu1, nu2, nu3 (times N: element offsets)
-  double w[6][32];   // matching half weights
+  int col[3][32];    // element offset (i0 * NS) of each stencil's first column
+  double w[6][32];   // 16 x half weights for columns i0 and i0 + 1 of nu1, nu2, nu3
   double phi[32];
   double invphi[32];  // 1/phi (0 when phi == 0: no fast span then)
   double pw[32];     // p1 * p2 * p3
   int src[32];       // chunk-local column of the listed point
   double val[32];    // pw * |kernel|^2 per chunk column
+  double nu, f, s1, s2, su, u1, lo, du2, row_acc;
 };
 
 // Polynomial coefficients as __constant__ data: ptxas keeps them in uniform
@@ -153,43 +156,43 @@ __device__ __forceinline__ void dev_sincos(double x, double* c_out, double* s_ou
 // shuffle per step serves every lane: lanes 0..14 receive p_{m+1} of the
 // same block; lane 15 receives lane 0's p of the current block, which is the
 // p_{m+1} of its own step from the previous block, whose term it deferred.
-// Slow branch (:176-188) is the direct sinc form.  Tables are padded past
-// the last step; lanes with m >= N mask p to 0 and feed sincos a 0 angle.
+// Slow branch (:176-188) is the direct sinc form.  Columns are NS = 16 K
+// doubles apart (padded), so a stencil's second column is an immediate offset
+// from its first; lanes with m >= N (only when N < NS) mask p to 0 and feed
+// sincos a 0 angle.
 template <int K, bool FULL>
 __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSmem& S, int idx,
                                                int probe, int sl, unsigned segmask,
                                                const double* tab) {
+  constexpr int NS = 16 * K;
   const int N = P.steps;
   const double phi = S.phi[idx];
   const double w0 = S.w[0][idx], w1 = S.w[1][idx], w2 = S.w[2][idx];
   const double w3 = S.w[3][idx], w4 = S.w[4][idx], w5 = S.w[5][idx];
-  const int o0 = S.col[0][idx] + sl, o1 = S.col[1][idx] + sl, o2 = S.col[2][idx] + sl;
-  const int o3 = S.col[3][idx] + sl, o4 = S.col[4][idx] + sl, o5 = S.col[5][idx] + sl;
+  const int oa = S.col[0][idx] + sl, ob = S.col[1][idx] + sl, oc = S.col[2][idx] + sl;
   const int rot = (sl + 1) & 15;
   double fre = 0.0, fim = 0.0, sre = 0.0, sim = 0.0;
   for (int k = 0; k < P.n_spans; ++k) {
     const double* T = P.log2rho + k * P.span_stride;
-    const double* c0 = T + o0;
-    const double* c1 = T + o1;
-    const double* c2 = T + o2;
-    const double* c3 = T + o3;
-    const double* c4 = T + o4;
-    const double* c5 = T + o5;
-    const double* hl = P.hl2 + (static_cast<size_t>(probe) * P.n_spans + k) * N + sl;
+    const double* ca = T + oa;
+    const double* cb = T + ob;
+    const double* cc3 = T + oc;
+    const double* hl = P.hl2 + (static_cast<size_t>(probe) * P.n_spans + k) * NS + sl;
     const bool fast = fabs(phi) * __ldg(P.wlast + k) > 1e-4;
     if (fast) {
-      const double* ze = P.zedge + static_cast<size_t>(k) * (N + 1) + 1 + sl;
+      const double* ze = P.zedge + static_cast<size_t>(k) * (NS + 1) + 1 + sl;
       const bool l15 = sl == 15;
       double pp = 0.0, pc = 0.0, ps = 0.0;  // previous block's (p, E): lane 15 defers
-      double pfirst = 0.0;
+      double c0v = 1.0, s0v = 0.0;          // E(z_0) of this span (1 for the first)
+      if (k > 0) dev_sincos(phi * __ldg(ze - 1 - sl), &c0v, &s0v);
 #pragma unroll
       for (int b = 0; b < K; ++b) {
-        double lg = fma(w0, __ldg(c0 + 16 * b), -__ldg(hl + 16 * b));
-        lg = fma(w1, __ldg(c1 + 16 * b), lg);
-        lg = fma(w2, __ldg(c2 + 16 * b), lg);
-        lg = fma(w3, __ldg(c3 + 16 * b), lg);
-        lg = fma(w4, __ldg(c4 + 16 * b), lg);
-        lg = fma(w5, __ldg(c5 + 16 * b), lg);
+        double lg = fma(w0, __ldg(ca + 16 * b), -__ldg(hl + 16 * b));
+        lg = fma(w1, __ldg(ca + NS + 16 * b), lg);
+        lg = fma(w2, __ldg(cb + 16 * b), lg);
+        lg = fma(w3, __ldg(cb + NS + 16 * b), lg);
+        lg = fma(w4, __ldg(cc3 + 16 * b), lg);
+        lg = fma(w5, __ldg(cc3 + NS + 16 * b), lg);
         double p = dev_exp2_16(lg, tab);
         double ang = phi * __ldg(ze + 16 * b);
         if (!FULL) {
@@ -197,41 +200,37 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
           p = ok ? p : 0.0;
           ang = ok ? ang : 0.0;
         }
-        if (b == 0) pfirst = p;
+        if (b == 0 && sl == 0) {  // -p_0 E(z_0)
+          fre = fma(-p, c0v, fre);
+          fim = fma(-p, s0v, fim);
+        }
         double cs, sn;
         dev_sincos(ang, &cs, &sn);
         const double pr = __shfl_sync(segmask, p, rot, 16);
         // lanes 0..14: (p_m - p_{m+1}) E_{m+1}; lane 15: the previous block's step
-        const double cc = (l15 ? pp : p) - pr;
-        fre = fma(cc, l15 ? pc : cs, fre);
-        fim = fma(cc, l15 ? ps : sn, fim);
+        const double cf = (l15 ? pp : p) - pr;
+        fre = fma(cf, l15 ? pc : cs, fre);
+        fim = fma(cf, l15 ? ps : sn, fim);
         pp = p;
         pc = cs;
         ps = sn;
       }
-      if (sl == 15) {  // p_N = 0
+      if (l15) {  // p_N = 0
         fre = fma(pp, pc, fre);
         fim = fma(pp, ps, fim);
       }
-      if (sl == 0) {  // -p_0 E(z_0)
-        const double z0 = __ldg(P.zedge + static_cast<size_t>(k) * (N + 1));
-        double c0v = 1.0, s0v = 0.0;
-        if (z0 != 0.0) dev_sincos(phi * z0, &c0v, &s0v);
-        fre = fma(-pfirst, c0v, fre);
-        fim = fma(-pfirst, s0v, fim);
-      }
     } else {
-      const double* zm = P.zmid + static_cast<size_t>(k) * N + sl;
-      const double* wd = P.width + static_cast<size_t>(k) * N + sl;
+      const double* zm = P.zmid + static_cast<size_t>(k) * NS + sl;
+      const double* wd = P.width + static_cast<size_t>(k) * NS + sl;
 #pragma unroll 1
       for (int b = 0; b < K; ++b) {
         if (sl + 16 * b < N) {
-          double lg = fma(w0, __ldg(c0 + 16 * b), -__ldg(hl + 16 * b));
-          lg = fma(w1, __ldg(c1 + 16 * b), lg);
-          lg = fma(w2, __ldg(c2 + 16 * b), lg);
-          lg = fma(w3, __ldg(c3 + 16 * b), lg);
-          lg = fma(w4, __ldg(c4 + 16 * b), lg);
-          lg = fma(w5, __ldg(c5 + 16 * b), lg);
+          double lg = fma(w0, __ldg(ca + 16 * b), -__ldg(hl + 16 * b));
+          lg = fma(w1, __ldg(ca + NS + 16 * b), lg);
+          lg = fma(w2, __ldg(cb + 16 * b), lg);
+          lg = fma(w3, __ldg(cb + NS + 16 * b), lg);
+          lg = fma(w4, __ldg(cc3 + 16 * b), lg);
+          lg = fma(w5, __ldg(cc3 + NS + 16 * b), lg);
           const double p = dev_exp2_16(lg, tab);
           const double wm = __ldg(wd + 16 * b);
           // sinc(x), |x| = |phi| w / 2 <= 5e-5 here: 1 - x^2/6 + x^4/120 is exact
@@ -266,6 +265,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
   if (threadIdx.x < 16) s_tab[threadIdx.x] = c_exp2_tab16[threadIdx.x];
   __syncthreads();
 
+  constexpr int NS = 16 * K;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int sl = lane & 15;
@@ -273,7 +273,6 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
   const unsigned segmask = 0xffffu << (16 * seg);
   WarpSmem& S = s_w[warp];
   const int per_probe = P.n_q * P.n_r;
-  const int N = P.steps;
 
   for (;;) {
     int row = 0;
@@ -281,47 +280,60 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
     row = __shfl_sync(kFull, row, 0);
     if (row >= P.total_rows) break;
     const int probe = row / per_probe;
-    const int rem = row - probe * per_probe;
-    const int q = rem / P.n_r + 1;
-    const int i = rem - (q - 1) * P.n_r;
-    const double nu = __ldg(P.probe_nu + probe);
-    const double f = nu - P.centre;
-
-    // quadrant_limits (gn_integral.hpp:63-79)
-    const double bm = P.half_band - f, bp = P.half_band + f;
-    double b1, b2, s1, s2;
-    switch (q) {
-      case 1: b1 = bm; b2 = bm; s1 = 1.0; s2 = 1.0; break;
-      case 2: b1 = bp; b2 = bm; s1 = -1.0; s2 = 1.0; break;
-      case 3: b1 = bp; b2 = bp; s1 = -1.0; s2 = -1.0; break;
-      default: b1 = bm; b2 = bp; s1 = 1.0; s2 = -1.0; break;
-    }
-    const double u1_max = b1 * b2;
-    if (!(u1_max > 0.0)) {
-      if (lane == 0) P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
-      continue;
-    }
-    // u1 bin (gn_integral.hpp:262-286)
     const int n_r = P.n_r;
-    double e0, e1;
-    if (P.u1_uniform) {
-      e0 = u1_max * static_cast<double>(i) / n_r;
-      e1 = u1_max * static_cast<double>(i + 1) / n_r;
-    } else {
-      e0 = i == 0 ? 0.0 : u1_max * exp(P.ln_min * static_cast<double>(n_r - i) / (n_r - 1));
-      e1 = u1_max * exp(P.ln_min * static_cast<double>(n_r - i - 1) / (n_r - 1));
+    double du1;
+    {
+      const int rem = row - probe * per_probe;
+      const int q = rem / n_r + 1;
+      const int i = rem - (q - 1) * n_r;
+      const double nu = __ldg(P.probe_nu + probe);
+      const double f = nu - P.centre;
+      // quadrant_limits (gn_integral.hpp:63-79)
+      const double bm = P.half_band - f, bp = P.half_band + f;
+      double b1, b2, s1, s2;
+      switch (q) {
+        case 1: b1 = bm; b2 = bm; s1 = 1.0; s2 = 1.0; break;
+        case 2: b1 = bp; b2 = bm; s1 = -1.0; s2 = 1.0; break;
+        case 3: b1 = bp; b2 = bp; s1 = -1.0; s2 = -1.0; break;
+        default: b1 = bm; b2 = bp; s1 = 1.0; s2 = -1.0; break;
+      }
+      const double u1_max = b1 * b2;
+      if (!(u1_max > 0.0)) {
+        if (lane == 0) P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
+        continue;
+      }
+      // u1 bin (gn_integral.hpp:262-286)
+      double e0, e1;
+      if (P.u1_uniform) {
+        e0 = u1_max * static_cast<double>(i) / n_r;
+        e1 = u1_max * static_cast<double>(i + 1) / n_r;
+      } else {
+        e0 = i == 0 ? 0.0 : u1_max * exp(P.ln_min * static_cast<double>(n_r - i) / (n_r - 1));
+        e1 = u1_max * exp(P.ln_min * static_cast<double>(n_r - i - 1) / (n_r - 1));
+      }
+      du1 = e1 - e0;
+      const double u1 = (e0 == 0.0 || P.u1_uniform) ? 0.5 * (e0 + e1) : sqrt(e0 * e1);
+      const double su = sqrt(u1);
+      const double hi = log(b1 / su);
+      const double lo = -log(b2 / su);
+      if (!(hi > lo)) {
+        if (lane == 0) P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
+        continue;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        S.nu = nu;
+        S.f = f;
+        S.s1 = s1;
+        S.s2 = s2;
+        S.su = su;
+        S.u1 = u1;
+        S.lo = lo;
+        S.du2 = (hi - lo) / n_r;
+        S.row_acc = 0.0;
+      }
+      __syncwarp();
     }
-    const double du1 = e1 - e0;
-    const double u1 = (e0 == 0.0 || P.u1_uniform) ? 0.5 * (e0 + e1) : sqrt(e0 * e1);
-    const double su = sqrt(u1);
-    const double hi = log(b1 / su);
-    const double lo = -log(b2 / su);
-    if (!(hi > lo)) {
-      if (lane == 0) P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
-      continue;
-    }
-    const double du2 = (hi - lo) / n_r;
-    double row_acc = 0.0;
     unsigned n_eval = 0;
 
     for (int jb = 0; jb < n_r; jb += 32) {
@@ -332,18 +344,19 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
       Stencil st1, st2, st3;
       double phi = 0.0, pw = 0.0;
       if (j < n_r) {
-        const double u2 = lo + (static_cast<double>(j) + 0.5) * du2;
+        const double nu = S.nu, su = S.su, u1 = S.u1;
+        const double u2 = S.lo + (static_cast<double>(j) + 0.5) * S.du2;
         const double g1 = su * exp(u2);
         const double g2 = u1 / g1;
-        const double f1 = s1 * g1;
-        const double f2 = s2 * g2;
+        const double f1 = S.s1 * g1;
+        const double f2 = S.s2 * g2;
         double p1, p2, p3;
         st1 = psd_and_stencil(P, nu + f1, &p1);
         st2 = psd_and_stencil(P, nu + f2, &p2);
         st3 = psd_and_stencil(P, nu + f1 + f2, &p3);
         active = p1 != 0.0 && p2 != 0.0 && p3 != 0.0;
         if (active) {
-          phi = phase_mismatch(f1, f2, f, P.beta2, P.beta3, P.beta4);
+          phi = phase_mismatch(f1, f2, S.f, P.beta2, P.beta3, P.beta4);
           pw = p1 * p2 * p3;
           fast = fabs(phi) * __ldg(P.wlast) > 1e-4;
         }
@@ -354,11 +367,13 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
       const unsigned lt = (1u << lane) - 1u;
       S.val[lane] = 0.0;
       if (active) {
-        // fast points first, then slow ones, so half-warp pairs rarely diverge
+        // fast points first, then slow ones, so half-warp pairs rarely diverge.
+        // Column i0 + 1 is always read: clamped stencils have hw1 = 0 and the
+        // table carries a zero pad column n.
         const int pos = fast ? __popc(fm & lt) : __popc(fm) + __popc(sm & lt);
-        S.col[0][pos] = st1.i0 * N; S.col[1][pos] = st1.i1 * N;
-        S.col[2][pos] = st2.i0 * N; S.col[3][pos] = st2.i1 * N;
-        S.col[4][pos] = st3.i0 * N; S.col[5][pos] = st3.i1 * N;
+        S.col[0][pos] = st1.i0 * NS;
+        S.col[1][pos] = st2.i0 * NS;
+        S.col[2][pos] = st3.i0 * NS;
         S.w[0][pos] = st1.hw0 * 16.0; S.w[1][pos] = st1.hw1 * 16.0;
         S.w[2][pos] = st2.hw0 * 16.0; S.w[3][pos] = st2.hw1 * 16.0;
         S.w[4][pos] = st3.hw0 * 16.0; S.w[5][pos] = st3.hw1 * 16.0;
@@ -377,12 +392,14 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
       __syncwarp();
       if (lane == 0) {
         const int lim = min(32, n_r - jb);
-        for (int t = 0; t < lim; ++t) row_acc += S.val[t];  // ascending j
+        double acc = S.row_acc;
+        for (int t = 0; t < lim; ++t) acc += S.val[t];  // ascending j
+        S.row_acc = acc;
       }
       __syncwarp();
     }
     if (lane == 0) {
-      P.rowsum[row] = row_acc * du1 * du2;
+      P.rowsum[row] = S.row_acc * du1 * S.du2;
       atomicAdd(P.n_eval, static_cast<unsigned long long>(n_eval));
     }
   }
@@ -395,13 +412,14 @@ __global__ void probe_halflog_kernel(const NliParams P) {
   const double nu = P.probe_nu[probe];
   double unused;
   const Stencil sc = psd_and_stencil(P, nu, &unused);
+  const int NS = P.col_stride;
   for (int k = 0; k < P.n_spans; ++k) {
     const double* T = P.log2rho + k * P.span_stride;
-    double* out = P.hl2 + (static_cast<size_t>(probe) * P.n_spans + k) * P.steps;
-    for (int m = threadIdx.x; m < P.steps; m += blockDim.x) {
+    double* out = P.hl2 + (static_cast<size_t>(probe) * P.n_spans + k) * NS;
+    for (int m = threadIdx.x; m < NS; m += blockDim.x) {
       // 16 x (the reference's half-log, in log2): the integrand works in 2^-4 log2 units
-      out[m] = 16.0 * (sc.hw0 * T[static_cast<size_t>(sc.i0) * P.steps + m] +
-                        sc.hw1 * T[static_cast<size_t>(sc.i1) * P.steps + m]);
+      out[m] = 16.0 * (sc.hw0 * T[static_cast<size_t>(sc.i0) * NS + m] +
+                       sc.hw1 * T[static_cast<size_t>(sc.i1) * NS + m]);
     }
   }
 }
@@ -540,7 +558,7 @@ int nli_ctas_per_sm(int steps) {
 int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaStream_t stream,
                cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
   RowKernel k = row_kernel_for(p.steps);
-  if (!k || p.n_probes <= 0) return -1;
+  if (!k || p.n_probes <= 0 || p.col_stride != 16 * ((p.steps + 15) / 16)) return -1;
   int launches = 0;
   cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), stream);
   cudaMemsetAsync(p.n_eval, 0, sizeof(unsigned long long), stream);

@@ -19,11 +19,12 @@ struct NliParams {
   // by log2 e so the integrand can use exp2), span-absolute edge/mid, widths.
   int n_spans;
   int steps;
-  const double* log2rho;  // [n_spans * n_ch * steps] (span k at k * span_stride)
-  size_t span_stride;     // n_ch * steps, or 0 when every span shares one table
-  const double* zedge;    // [n_spans * (steps + 1)] = z_base + edge
-  const double* zmid;     // [n_spans * steps]       = z_base + mid
-  const double* width;    // [n_spans * steps]
+  int col_stride;         // NS = 16 * ceil(steps / 16): padded column length (doubles)
+  const double* log2rho;  // [n_spans][n_ch + 1][NS]: log2 rho, zero pad column n and pad steps
+  size_t span_stride;     // (n_ch + 1) * NS, or 0 when every span shares one table
+  const double* zedge;    // [n_spans][NS + 1] = z_base + edge (edges past N repeat L)
+  const double* zmid;     // [n_spans][NS]     = z_base + mid
+  const double* width;    // [n_spans][NS]
   const double* wlast;    // [n_spans] width.back(): fast/slow switch (gn_integral.hpp:156)
   double beta2, beta3, beta4;
   // GnSolverConfig
@@ -34,7 +35,7 @@ struct NliParams {
   // probes
   int n_probes;
   const double* probe_nu;  // [n_probes]
-  double* hl2;             // [n_probes * n_spans * steps] log2 half-power of the probe
+  double* hl2;             // [n_probes][n_spans][NS] 16 x log2 half-power of the probe
   // work queue + outputs
   int total_rows;               // n_probes * n_q * n_r
   unsigned int* counter;        // row queue head (zeroed before launch)

@@ -14,6 +14,7 @@ struct OdeParams {
   const int* row_lo;     // [n] first nonzero column of row i
   const int* row_hi;     // [n] one past the last nonzero column
   int steps;             // distance-grid steps (midpoints)
+  int col_stride;        // row stride of log2rho / log_rho (>= steps)
   const double* mid;     // [steps]
   double length;
   double rtol, atol;

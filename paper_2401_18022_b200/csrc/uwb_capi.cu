@@ -67,28 +67,35 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   if (steps < 1 || steps > kMaxSteps)
     return fail(UWB_CONFIG_ERROR, "uwb: distance steps per span must be in [1, 256]");
 
-  std::vector<double> tab(static_cast<size_t>(n_spans) * n * steps);
-  std::vector<double> ze(static_cast<size_t>(n_spans) * (steps + 1));
-  std::vector<double> zm(static_cast<size_t>(n_spans) * steps);
-  std::vector<double> wd(static_cast<size_t>(n_spans) * steps);
+  // Padded device layout (nli_kernel.cuh): columns NS = 16 ceil(N/16) long,
+  // one zero pad column n per span, edges past N repeat the span end.
+  const int NS = 16 * ((steps + 15) / 16);
+  const size_t cols = static_cast<size_t>(n + 1) * NS;
+  std::vector<double> tab(static_cast<size_t>(n_spans) * cols, 0.0);
+  std::vector<double> ze(static_cast<size_t>(n_spans) * (NS + 1));
+  std::vector<double> zm(static_cast<size_t>(n_spans) * NS);
+  std::vector<double> wd(static_cast<size_t>(n_spans) * NS);
   std::vector<double> wl(n_spans);
   double z_base = 0.0;
   for (int k = 0; k < n_spans; ++k) {
     const uwb_span& s = spans[k];
-    double* t = tab.data() + static_cast<size_t>(k) * n * steps;
-    for (size_t x = 0; x < static_cast<size_t>(n) * steps; ++x) t[x] = s.log_rho[x] * kLog2e;
-    for (int m = 0; m <= steps; ++m) ze[static_cast<size_t>(k) * (steps + 1) + m] = z_base + s.edge[m];
-    for (int m = 0; m < steps; ++m) {
-      zm[static_cast<size_t>(k) * steps + m] = z_base + s.mid[m];
-      wd[static_cast<size_t>(k) * steps + m] = s.width[m];
+    double* t = tab.data() + static_cast<size_t>(k) * cols;
+    for (int ch = 0; ch < n; ++ch)
+      for (int m = 0; m < steps; ++m)
+        t[static_cast<size_t>(ch) * NS + m] = s.log_rho[static_cast<size_t>(ch) * steps + m] * kLog2e;
+    for (int m = 0; m <= NS; ++m)
+      ze[static_cast<size_t>(k) * (NS + 1) + m] = z_base + s.edge[std::min(m, steps)];
+    for (int m = 0; m < NS; ++m) {
+      zm[static_cast<size_t>(k) * NS + m] = z_base + s.mid[std::min(m, steps - 1)];
+      wd[static_cast<size_t>(k) * NS + m] = s.width[std::min(m, steps - 1)];
     }
     wl[k] = s.width[steps - 1];
     z_base += s.length;
   }
   double* d_freq = c->freq.get<double>(n);
   double* d_psd = c->psd.get<double>(n);
-  double* d_tab = c->log2rho.get<double>(tab.size() + kTablePad);  // lanes past N read the pad
-  double* d_ze = c->zedge.get<double>(ze.size() + kTablePad);
+  double* d_tab = c->log2rho.get<double>(tab.size());
+  double* d_ze = c->zedge.get<double>(ze.size());
   double* d_zm = c->zmid.get<double>(zm.size());
   double* d_wd = c->width.get<double>(wd.size());
   double* d_wl = c->wlast.get<double>(wl.size());
@@ -116,7 +123,8 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   P->n_spans = n_spans;
   P->steps = steps;
   P->log2rho = d_tab;
-  P->span_stride = static_cast<size_t>(n) * steps;
+  P->col_stride = NS;
+  P->span_stride = cols;
   P->zedge = d_ze;
   P->zmid = d_zm;
   P->width = d_wd;
@@ -164,7 +172,7 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
   P.n_probes = np;
   P.total_rows = np * P.n_q * P.n_r;
   P.probe_nu = d_nu;
-  P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * P.steps + kTablePad);
+  P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * P.col_stride);
   P.rowsum = c->rowsum.get<double>(std::max(P.total_rows, 1));
   P.counter = c->counter.get<unsigned int>(1);
   P.n_eval = c->n_eval.get<unsigned long long>(1);

@@ -235,14 +235,16 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   std::vector<int> band(n, -1);
   if (lk->band) std::copy(lk->band, lk->band + n, band.begin());
   const double* d_mid = up(c, c->mid, mid.data(), mid.size());
-  // span-absolute grids: every span is a copy of the one evolution (solve_link_noise :185)
+  // span-absolute grids: every span is a copy of the one evolution
+  // (solve_link_noise :185); padded layout of nli_kernel.cuh
+  const int NS = 16 * ((steps + 15) / 16);
   std::vector<double> ze, zm, wd, wl;
   double z_base = 0.0;
   for (int k = 0; k < fb->span_count; ++k) {
-    for (int m = 0; m <= steps; ++m) ze.push_back(z_base + edge[m]);
-    for (int m = 0; m < steps; ++m) {
-      zm.push_back(z_base + mid[m]);
-      wd.push_back(width[m]);
+    for (int m = 0; m <= NS; ++m) ze.push_back(z_base + edge[std::min(m, steps)]);
+    for (int m = 0; m < NS; ++m) {
+      zm.push_back(z_base + mid[std::min(m, steps - 1)]);
+      wd.push_back(width[std::min(m, steps - 1)]);
     }
     wl.push_back(width[steps - 1]);
     z_base += fb->length_m;
@@ -256,9 +258,11 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   P.half_band = g->half_band;
   P.n_spans = fb->span_count;
   P.steps = steps;
-  P.log2rho = c->log2rho.get<double>(static_cast<size_t>(n) * steps + kTablePad);
+  const size_t cols = static_cast<size_t>(n + 1) * NS;
+  P.log2rho = c->log2rho.get<double>(cols);
+  cudaMemsetAsync(const_cast<double*>(P.log2rho), 0, cols * sizeof(double), c->stream);  // pads
+  P.col_stride = NS;
   P.span_stride = 0;
-  ze.resize(ze.size() + kTablePad, 0.0);  // lanes past N read the pad
   P.zedge = up(c, c->zedge, ze.data(), ze.size());
   P.zmid = up(c, c->zmid, zm.data(), zm.size());
   P.width = up(c, c->width, wd.data(), wd.size());
@@ -280,7 +284,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   P.n_probes = np;
   P.total_rows = np * P.n_q * P.n_r;
   P.probe_nu = up(c, c->probe_nu, nu.data(), nu.size());
-  P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * steps + kTablePad);
+  P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * NS);
   P.rowsum = c->rowsum.get<double>(std::max(P.total_rows, 1));
   P.counter = c->counter.get<unsigned int>(1);
   P.n_eval = c->n_eval.get<unsigned long long>(1);
@@ -322,6 +326,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   O.row_lo = pr->d_lo;
   O.row_hi = pr->d_hi;
   O.steps = steps;
+  O.col_stride = NS;
   O.mid = d_mid;
   O.length = fb->length_m;
   O.rtol = pr->rtol;
@@ -565,6 +570,7 @@ int uwb_power_evolution(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre
   O.row_lo = d_lo;
   O.row_hi = d_lo + n;
   O.steps = steps;
+  O.col_stride = steps;
   O.mid = d_mid;
   O.length = fibre->length_m;
   O.rtol = link->rtol > 0 ? link->rtol : 1e-9;
