@@ -7,32 +7,41 @@
 
 namespace uwb {
 
+constexpr int kMaxOdeChannels = 2560;  // 640 threads x 4 channels per thread
+constexpr int kMaxRamanSegments = 4;  // linear pieces of the gain table in d = |j - i|
+
 struct OdeParams {
   int n;                 // channels
+  int raman;             // RamanSolveOptions::include_raman
   const double* alpha;   // [n] 1/m
-  const double* M;       // [n*n] coupling premultiplied by launch power, or null (Raman off)
-  const int* row_lo;     // [n] first nonzero column of row i
-  const int* row_hi;     // [n] one past the last nonzero column
+  double* coef_a;        // [n] f_i aeff_ref / aeff_i          (filled on device)
+  double* coef_u;        // [n] P_i / f_i                      (filled on device)
+  double* coef_v;        // [n] aeff_ref P_i / aeff_i          (filled on device)
+  int n_seg;             // gain table as G = a + b d on d in [dlo, dhi]
+  int seg_dlo[kMaxRamanSegments];
+  int seg_dhi[kMaxRamanSegments];
+  double seg_a[kMaxRamanSegments];
+  double seg_b[kMaxRamanSegments];
   int steps;             // distance-grid steps (midpoints)
   int col_stride;        // row stride of log2rho / log_rho (>= steps)
   const double* mid;     // [steps]
   double length;
   double rtol, atol;
-  double* log2rho;       // [n*steps] out: log2(rho) in the NLI layout
-  double* log_rho;       // [n*steps] out: ln(rho) (may be null)
+  double* log2rho;       // [n * col_stride] out: log2(rho) in the NLI layout
+  double* log_rho;       // [n * col_stride] out: ln(rho) (may be null)
   double* rho_end;       // [n] out
   int* status;           // out: 0 ok, 1 non-positive rho, 2 step budget, 3 step underflow
   long long* rhs_evals;  // out (may be null)
-  int rows_per_cta;      // set by launch_raman_ode
-  int slab_in_smem;      // set by launch_raman_ode
 };
 
-// Builds M (if P.M != null) from the grid/fibre arrays and runs the cluster
-// ODE kernel.  Returns kernel launches issued, or < 0 on a launch failure.
-int launch_raman_ode(OdeParams P, const double* freq, const double* psd, double bch,
-                     const double* aeff, const double* rx, const double* ry, int rn,
-                     double aeff_ref, double* M, int* row_lo, int* row_hi, cudaStream_t st);
+// Gain table (x, y) -> d-segments for channel spacing `spacing` (host).
+// Returns 0, or -1 if the table does not fit kMaxRamanSegments.
+int raman_segments(const double* x, const double* y, int rn, double spacing, int n_ch,
+                   OdeParams* P);
 
-size_t ode_smem_bytes(int n, int rpc, bool slab);
+// Fills the per-channel coupling factors from the launch PSD and runs the
+// one-CTA ODE kernel.  Returns kernel launches issued, or < 0 on failure.
+int launch_raman_ode(OdeParams P, const double* freq, const double* psd, double bch,
+                     const double* aeff, double aeff_ref, cudaStream_t st);
 
 }  // namespace uwb

@@ -169,11 +169,6 @@ struct uwb_ctx::Prepared {
   int raman_n = 0;
   double aeff_ref = 0.0;
   const double* d_aeff = nullptr;
-  const double* d_rx = nullptr;
-  const double* d_ry = nullptr;
-  double* d_M = nullptr;
-  int* d_lo = nullptr;
-  int* d_hi = nullptr;
   int* d_status = nullptr;
   long long* d_rhs = nullptr;
   double* d_psd = nullptr;  // the NLI/ODE/link read launch PSD from here
@@ -227,8 +222,6 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   const uint8_t* d_guard = up(c, c->guard, g->guard, n);
   const double* d_alpha = up(c, c->alpha, fb->alpha, n);
   pr->d_aeff = up(c, c->aeff, fb->aeff, n);
-  pr->d_rx = up(c, c->raman_x, fb->raman_x, fb->raman_n);
-  pr->d_ry = up(c, c->raman_y, fb->raman_y, fb->raman_n);
   pr->raman_n = fb->raman_n;
   pr->aeff_ref = fb->raman_aeff_ref;
   const double* d_nf = up(c, c->nf_db, lk->nf_db, n);
@@ -305,26 +298,25 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   F.quad = c->quad.get<double>(4 * n);
   F.skipped = c->skipped.get<uint8_t>(n);
 
-  // ODE
+  // ODE (raman_ode.cu): separable coupling factors + gain-table segments
   OdeParams& O = pr->O;
   O.n = n;
+  O.raman = lk->include_raman ? 1 : 0;
   O.alpha = d_alpha;
-  // ode_work: M [n*n] | rho_end [n] | status | rhs | row_lo [n] | row_hi [n] | band [n] | link tmp [3n]
-  const size_t nn = static_cast<size_t>(n) * n;
-  double* w = c->ode_work.get<double>(nn + n + 2 + 3 * n + 3 * n + 8);
+  if (O.raman && raman_segments(fb->raman_x, fb->raman_y, fb->raman_n, g->spacing, n, &O))
+    return fail(UWB_CONFIG_ERROR, "raman gain table has too many linear pieces");
+  if (n > kMaxOdeChannels) return fail(UWB_CONFIG_ERROR, "uwb: at most 2560 channels");
+  // ode_work: coef a|u|v [3n] | rho_end [n] | status, rhs [2] | band [n ints] | link tmp [3n]
+  double* w = c->ode_work.get<double>(3 * static_cast<size_t>(n) + n + 2 + n + 3 * n + 8);
   if (!w) return fail(UWB_CUDA_ERROR, "device allocation failed");
-  pr->d_M = w;
-  O.M = lk->include_raman ? pr->d_M : nullptr;
-  double* d_rho_end = w + nn;
-  pr->d_status = reinterpret_cast<int*>(w + nn + n);
-  pr->d_rhs = reinterpret_cast<long long*>(w + nn + n + 1);
-  int* ip = reinterpret_cast<int*>(w + nn + n + 2);
-  pr->d_lo = ip;
-  pr->d_hi = ip + n;
-  int* d_band2 = ip + 2 * n;
-  double* d_tmp = w + nn + n + 2 + 2 * n;  // 3n ints fit in 1.5n doubles; start tmp after 2n
-  O.row_lo = pr->d_lo;
-  O.row_hi = pr->d_hi;
+  O.coef_a = w;
+  O.coef_u = w + n;
+  O.coef_v = w + 2 * n;
+  double* d_rho_end = w + 3 * n;
+  pr->d_status = reinterpret_cast<int*>(w + 4 * n);
+  pr->d_rhs = reinterpret_cast<long long*>(w + 4 * n + 1);
+  int* d_band2 = reinterpret_cast<int*>(w + 4 * n + 2);
+  double* d_tmp = w + 5 * n + 2;
   O.steps = steps;
   O.col_stride = NS;
   O.mid = d_mid;
@@ -374,10 +366,9 @@ int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st) {
     xfer(c, pr->d_psd, psd_dev, pr->n * sizeof(double), cudaMemcpyDeviceToDevice, st);
   cudaMemsetAsync(pr->d_status, 0, sizeof(int), st);
   cudaEventRecord(c->ev0, st);
-  const int lo = launch_raman_ode(pr->O, pr->P.freq, pr->d_psd, pr->P.bch, pr->d_aeff, pr->d_rx,
-                                  pr->d_ry, pr->raman_n, pr->aeff_ref, pr->d_M, pr->d_lo,
-                                  pr->d_hi, st);
-  if (lo < 0) return fail(UWB_CUDA_ERROR, "raman ODE launch failed (cluster/smem)");
+  const int lo = launch_raman_ode(pr->O, pr->P.freq, pr->d_psd, pr->P.bch, pr->d_aeff,
+                                  pr->aeff_ref, st);
+  if (lo < 0) return fail(UWB_CUDA_ERROR, "raman ODE launch failed");
   launches += lo;
   if (pr->P.n_probes > 0) {
     const int ln = launch_nli(pr->P, pr->F, pr->grid_ctas, st, c->evk0, c->evk1);
@@ -551,24 +542,28 @@ int uwb_power_evolution(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre
   const double* d_psd = up(c, c->psd, grid->psd, n);
   const double* d_alpha = up(c, c->alpha, fibre->alpha, n);
   const double* d_aeff = up(c, c->aeff, fibre->aeff, n);
-  const double* d_rx = up(c, c->raman_x, fibre->raman_x, fibre->raman_n);
-  const double* d_ry = up(c, c->raman_y, fibre->raman_y, fibre->raman_n);
   const double* d_mid = up(c, c->mid, mid, steps);
-  const size_t nn = static_cast<size_t>(n) * n;
-  double* w = c->ode_work.get<double>(nn + 2 * static_cast<size_t>(n) * steps + n + 2 + 2 * n);
+  if (link->include_raman && (fibre->raman_n < 2 || !fibre->raman_x || !fibre->raman_y))
+    return fail(UWB_CONFIG_ERROR, "raman gain: table needs at least two (x, y) rows");
+  if (n > kMaxOdeChannels) return fail(UWB_CONFIG_ERROR, "uwb: at most 2560 channels");
+  // ode_work: log2 [n*steps] | ln [n*steps] | rho_end [n] | status, rhs [2] | coef a|u|v [3n]
+  const size_t ns = static_cast<size_t>(n) * steps;
+  double* w = c->ode_work.get<double>(2 * ns + n + 2 + 3 * n);
   if (!w) return fail(UWB_CUDA_ERROR, "device allocation failed");
   OdeParams O{};
   O.n = n;
+  O.raman = link->include_raman ? 1 : 0;
   O.alpha = d_alpha;
-  O.M = link->include_raman ? w : nullptr;
-  double* d_l2 = w + nn;
-  double* d_ln = d_l2 + static_cast<size_t>(n) * steps;
-  double* d_re = d_ln + static_cast<size_t>(n) * steps;
+  if (O.raman && raman_segments(fibre->raman_x, fibre->raman_y, fibre->raman_n, grid->spacing, n, &O))
+    return fail(UWB_CONFIG_ERROR, "raman gain table has too many linear pieces");
+  double* d_l2 = w;
+  double* d_ln = w + ns;
+  double* d_re = w + 2 * ns;
   int* d_status = reinterpret_cast<int*>(d_re + n);
   long long* d_rhs = reinterpret_cast<long long*>(d_re + n + 1);
-  int* d_lo = reinterpret_cast<int*>(d_re + n + 2);
-  O.row_lo = d_lo;
-  O.row_hi = d_lo + n;
+  O.coef_a = d_re + n + 2;
+  O.coef_u = O.coef_a + n;
+  O.coef_v = O.coef_u + n;
   O.steps = steps;
   O.col_stride = steps;
   O.mid = d_mid;
@@ -580,12 +575,9 @@ int uwb_power_evolution(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre
   O.rho_end = d_re;
   O.status = d_status;
   O.rhs_evals = d_rhs;
-  if (fibre->raman_n < 2 && link->include_raman)
-    return fail(UWB_CONFIG_ERROR, "raman gain: table needs at least two (x, y) rows");
   cudaMemsetAsync(d_status, 0, sizeof(int), st);
-  const int lo = launch_raman_ode(O, d_freq, d_psd, grid->bch, d_aeff, d_rx, d_ry, fibre->raman_n,
-                                  fibre->raman_aeff_ref, w, d_lo, d_lo + n, st);
-  if (lo < 0) return fail(UWB_CUDA_ERROR, "raman ODE launch failed (cluster/smem)");
+  const int lo = launch_raman_ode(O, d_freq, d_psd, grid->bch, d_aeff, fibre->raman_aeff_ref, st);
+  if (lo < 0) return fail(UWB_CUDA_ERROR, "raman ODE launch failed");
   c->last_launches = lo;
   if (log_rho) xfer(c, log_rho, d_ln, static_cast<size_t>(n) * steps * 8, cudaMemcpyDeviceToHost, st);
   if (rho_end) xfer(c, rho_end, d_re, n * 8, cudaMemcpyDeviceToHost, st);
