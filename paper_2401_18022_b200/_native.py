@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libuwbnli.so")
+LIB_PATH = os.environ.get("UWB_LIB_PATH", os.path.join(PKG, "libuwbnli.so"))
 
 DP = C.POINTER(C.c_double)
 IP = C.POINTER(C.c_int)

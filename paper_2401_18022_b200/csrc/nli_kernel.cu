@@ -106,9 +106,13 @@ __constant__ double c_sin[6] = {kS1, kS2, kS3, kS4, kS5, kS6};
 __constant__ double c_cos[6] = {kC1, kC2, kC3, kC4, kC5, kC6};
 __constant__ double c_red[3] = {kTwoOverPi, -kPio2Hi, -kPio2Lo};
 
+// 2^(j/16) for dev_exp2_16, filled by each CTA at start.  A file-scope
+// __shared__ array (not a generic pointer) so the lookup is one LDS.
+__shared__ double s_exp2_tab[16];
+
 // 2^(x/16), x = 16 log2 p (uwb_devmath.cuh exp2_16): 3 DADD + 7 DFMA + 1 DMUL,
 // one conflict-free LDS.
-__device__ __forceinline__ double dev_exp2_16(double x, const double* tab) {
+__device__ __forceinline__ double dev_exp2_16(double x) {
   const double t = x + kMagic;
   const int k = __double2loint(t);
   const double r = x - (t - kMagic);
@@ -119,7 +123,7 @@ __device__ __forceinline__ double dev_exp2_16(double x, const double* tab) {
   p = fma(p, r, c_e4[1]);
   p = fma(p, r, c_e4[0]);
   p = fma(p, r, 1.0);
-  const double s = tab[k & 15] * p;
+  const double s = s_exp2_tab[k & 15] * p;
   return __hiloint2double(__double2hiint(s) + ((k >> 4) << 20), __double2loint(s));
 }
 
@@ -162,8 +166,7 @@ __device__ __forceinline__ void dev_sincos(double x, double* c_out, double* s_ou
 // sincos a 0 angle.
 template <int K, bool FULL>
 __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSmem& S, int idx,
-                                               int probe, int sl, unsigned segmask,
-                                               const double* tab) {
+                                               int probe, int sl, unsigned segmask) {
   constexpr int NS = 16 * K;
   const int N = P.steps;
   const double phi = S.phi[idx];
@@ -185,16 +188,31 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
       double pp = 0.0, pc = 0.0, ps = 0.0;  // previous block's (p, E): lane 15 defers
       double c0v = 1.0, s0v = 0.0;          // E(z_0) of this span (1 for the first)
       if (k > 0) dev_sincos(phi * __ldg(ze - 1 - sl), &c0v, &s0v);
+      // one step block ahead: the 8 loads of block b + 1 are in flight while
+      // block b computes (L1 hits ~35 cycles, the ~22 % L2 hits ~300)
+      double l0 = __ldg(ca), l1 = __ldg(ca + NS), l2 = __ldg(cb), l3 = __ldg(cb + NS);
+      double l4 = __ldg(cc3), l5 = __ldg(cc3 + NS), lh = __ldg(hl), lz = __ldg(ze);
 #pragma unroll
       for (int b = 0; b < K; ++b) {
-        double lg = fma(w0, __ldg(ca + 16 * b), -__ldg(hl + 16 * b));
-        lg = fma(w1, __ldg(ca + NS + 16 * b), lg);
-        lg = fma(w2, __ldg(cb + 16 * b), lg);
-        lg = fma(w3, __ldg(cb + NS + 16 * b), lg);
-        lg = fma(w4, __ldg(cc3 + 16 * b), lg);
-        lg = fma(w5, __ldg(cc3 + NS + 16 * b), lg);
-        double p = dev_exp2_16(lg, tab);
-        double ang = phi * __ldg(ze + 16 * b);
+        double lg = fma(w0, l0, -lh);
+        lg = fma(w1, l1, lg);
+        lg = fma(w2, l2, lg);
+        lg = fma(w3, l3, lg);
+        lg = fma(w4, l4, lg);
+        lg = fma(w5, l5, lg);
+        double ang = phi * lz;
+        if (b + 1 < K) {
+          const int o = 16 * (b + 1);
+          l0 = __ldg(ca + o);
+          l1 = __ldg(ca + NS + o);
+          l2 = __ldg(cb + o);
+          l3 = __ldg(cb + NS + o);
+          l4 = __ldg(cc3 + o);
+          l5 = __ldg(cc3 + NS + o);
+          lh = __ldg(hl + o);
+          lz = __ldg(ze + o);
+        }
+        double p = dev_exp2_16(lg);
         if (!FULL) {
           const bool ok = sl + 16 * b < N;
           p = ok ? p : 0.0;
@@ -231,7 +249,7 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
           lg = fma(w3, __ldg(cb + NS + 16 * b), lg);
           lg = fma(w4, __ldg(cc3 + 16 * b), lg);
           lg = fma(w5, __ldg(cc3 + NS + 16 * b), lg);
-          const double p = dev_exp2_16(lg, tab);
+          const double p = dev_exp2_16(lg);
           const double wm = __ldg(wd + 16 * b);
           // sinc(x), |x| = |phi| w / 2 <= 5e-5 here: 1 - x^2/6 + x^4/120 is exact
           const double x = 0.5 * phi * wm;
@@ -260,9 +278,8 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
 
 template <int K, bool FULL>
 __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParams P) {
-  __shared__ double s_tab[16];
   __shared__ WarpSmem s_w[kWarps];
-  if (threadIdx.x < 16) s_tab[threadIdx.x] = c_exp2_tab16[threadIdx.x];
+  if (threadIdx.x < 16) s_exp2_tab[threadIdx.x] = c_exp2_tab16[threadIdx.x];
   __syncthreads();
 
   constexpr int NS = 16 * K;
@@ -386,7 +403,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
       const int n_act = __popc(am);
       n_eval += n_act;
       for (int idx = seg; idx < n_act; idx += 2) {
-        const double kv = point_kernel<K, FULL>(P, S, idx, probe, sl, segmask, s_tab);
+        const double kv = point_kernel<K, FULL>(P, S, idx, probe, sl, segmask);
         if (sl == 0) S.val[S.src[idx]] = S.pw[idx] * kv;
       }
       __syncwarp();
