@@ -188,6 +188,7 @@ def run_engine(args):
     import torch.distributed as dist
 
     import paper_2401_18022_b200 as uwb
+    from paper_2401_18022_b200.multigpu import ShardedLink
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -202,34 +203,19 @@ def run_engine(args):
     fibre = uwb.default_fibre()
     gn = uwb.GnSolverConfig(n_r=args.n_r, mean_step_density=args.density)
     lc = uwb.LinkConfig(gn=gn)
-    active = np.flatnonzero((grid.guard == 0) & (grid.psd > 0))
-    mine = active[rank::world] if world > 1 else None
-    if mine is not None:
-        eng.set_channel_subset(mine)
-
     # a real (non-legacy) stream: the C-ABI maps a NULL stream to its own
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
-    res = uwb.ResidentLink(fibre, grid, lc, engine=eng)
+    sh = ShardedLink(fibre, grid, lc, rank, world, engine=eng)
+    res = sh.res
     psd = torch.tensor(grid.psd, dtype=torch.float64, device=dev)
-    report = torch.zeros(res.report_len, dtype=torch.float64, device=dev)
-    eta_ptr, n_ch = res.eta_buffer()
-
-    class _Cai:  # zero-copy torch view of the engine's eta buffer for NCCL
-        __cuda_array_interface__ = {"shape": (n_ch,), "typestr": "<f8", "data": (eta_ptr, False),
-                                    "version": 3}
-
-    eta_view = torch.as_tensor(_Cai(), device=dev)
+    report = torch.zeros(sh.report_len, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    n_launch = [0]
 
     def step():
-        if world == 1:
-            res.run(psd.data_ptr(), report.data_ptr(), sp)
-        else:
-            res.run_noise(psd.data_ptr(), sp)
-            dist.all_reduce(eta_view, op=dist.ReduceOp.SUM)
-            res.run_report(report.data_ptr(), sp)
+        n_launch[0] = sh.run(psd.data_ptr(), report.data_ptr(), sp)
 
     def barrier():
         if world > 1:
@@ -253,7 +239,7 @@ def run_engine(args):
             step()
             ev[k][1].record(stream)
             torch.cuda.synchronize(dev)
-            launches += eng.last_launches() + (2 if world > 1 else 0)
+            launches += n_launch[0]
             kern_ms.append(eng.last_nli_stats()["kernel_ms"])
         barrier()
     res.check_status()
@@ -346,7 +332,9 @@ def run_engine(args):
                    "sample": f"failed: {e}"}
 
     if rank == 0:
-        achieved = FLOPS_PER_STEP * inner / (kmax * 1e-3) / 1e12 if kmax > 0 else None
+        # per-GPU achieved rate of the integrand kernel (all ranks' steps over
+        # the slowest rank's kernel time, divided by the GPU count)
+        achieved = FLOPS_PER_STEP * inner / (kmax * 1e-3) / 1e12 / world if kmax > 0 else None
         tr = read_traffic()
         line = {
             "metric": METRIC, "value": ms_per / 1e3, "unit": UNIT, "n_gpus": world,

@@ -1,0 +1,84 @@
+"""CPU, world_size 2 over gloo: the multi-GPU data path's host logic.
+
+Each rank evaluates only its partition of the channels (here with the oracle
+standing in for the GPU kernel -- test-only), the per-rank eta vectors are
+combined by the same allreduce_eta the bench uses, and the result must be
+bit-identical to a single-process run (the reference's bit-identity across
+worker counts, test_gn_integral.cpp:291-300)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2401_18022_b200.multigpu import active_channels, allreduce_eta, partition_channels
+
+
+def test_partition_covers_and_balances():
+    ch = np.arange(557)
+    for world in (1, 2, 3, 4, 8):
+        parts = partition_channels(ch, world)
+        allc = np.sort(np.concatenate(parts))
+        assert np.array_equal(allc, ch)
+        sizes = [len(p) for p in parts]
+        assert max(sizes) - min(sizes) <= 1
+    cost = np.linspace(1.0, 1.32, 557)  # O-band edge COIs are heavier
+    parts = partition_channels(ch, 8, cost)
+    loads = [cost[np.isin(ch, p)].sum() for p in parts]
+    assert max(loads) / min(loads) < 1.02  # one item of granularity
+    assert np.array_equal(np.sort(np.concatenate(parts)), ch)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.join(os.path.dirname(here), "oracle"))
+    from pyoracle import Oracle, cband11
+
+    O = Oracle()
+    case = cband11(n_r=24, density=0.95, workers=1)
+    prep = O.prepare(case)
+    ga = prep["grid_arrays"]
+
+    class G:
+        guard = ga["guard"]
+        psd = ga["psd"]
+
+    mine = partition_channels(active_channels(G), world)[rank]
+    full = O.all_channels_nli(case, prep)
+    eta = torch.zeros(len(ga["freq"]), dtype=torch.float64)
+    # rank-local evaluation: only this rank's channels are non-zero
+    eta[mine] = torch.from_numpy(full["eta"][mine])
+    allreduce_eta(eta)
+    if rank == 0:
+        q.put((eta.numpy().copy(), full["eta"]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_allreduce_is_bit_identical():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got, want = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert np.array_equal(got, want)
