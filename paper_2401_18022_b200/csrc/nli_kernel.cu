@@ -31,6 +31,7 @@
 #include <cstdint>
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "nli_kernel.cuh"
 #include "uwb_devmath.cuh"
@@ -155,27 +156,31 @@ __device__ __forceinline__ void dev_sincos(double x, double* c_out, double* s_ou
 }
 
 // |sum over spans & steps|^2 for one point, computed by one 16-lane segment.
-// Step m = sl + 16 b.  Fast branch (gn_integral.hpp:156-175) by summation by
-// parts: the lane of step m adds (p_m - p_{m+1}) E(z_{m+1}).  One rotating
-// shuffle per step serves every lane: lanes 0..14 receive p_{m+1} of the
-// same block; lane 15 receives lane 0's p of the current block, which is the
-// p_{m+1} of its own step from the previous block, whose term it deferred.
-// Slow branch (:176-188) is the direct sinc form.  Columns are NS = 16 K
-// doubles apart (padded), so a stencil's second column is an immediate offset
-// from its first; lanes with m >= N (only when N < NS) mask p to 0 and feed
-// sincos a 0 angle.
-template <int K, bool FULL>
+// Lane sl owns the K consecutive steps m = sl K + b (lane_pos layout, so for
+// each b the segment's 16 loads of a column are one 128-byte line).
+// Fast branch (gn_integral.hpp:156-175) by summation by parts of the
+// reference's phasor-difference sum:
+//   sum_m p_m (E_{m+1} - E_m) = -p_0 E_0 + sum_{m} (p_m - p_{m+1}) E_{m+1}
+// (p_N = 0): step b adds (p_{b-1} - p_b) E_b of the previous step, the
+// lane's last step pairs with the next lane's first p (one shuffle per point),
+// so each step costs one exp2 and one sincos and nothing crosses lanes inside
+// the step loop.  Slow branch (:176-188) is the direct sinc form.  Lanes with
+// m >= N (only when N < 16 K) mask p to 0 and feed sincos a 0 angle.
+// HOIST: the lane's K end-edge positions Zr and probe half-logs Hr live in
+// registers for the whole row (single span, K <= 8).
+template <int K, bool FULL, bool HOIST>
 __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSmem& S, int idx,
-                                               int probe, int sl, unsigned segmask) {
+                                               int probe, int sl, unsigned segmask,
+                                               const double (&Zr)[K], const double (&Hr)[K]) {
   constexpr int NS = 16 * K;
   const int N = P.steps;
   const double phi = S.phi[idx];
   const double w0 = S.w[0][idx], w1 = S.w[1][idx], w2 = S.w[2][idx];
   const double w3 = S.w[3][idx], w4 = S.w[4][idx], w5 = S.w[5][idx];
   const int oa = S.col[0][idx] + sl, ob = S.col[1][idx] + sl, oc = S.col[2][idx] + sl;
-  const int rot = (sl + 1) & 15;
   double fre = 0.0, fim = 0.0, sre = 0.0, sim = 0.0;
-  for (int k = 0; k < P.n_spans; ++k) {
+  const int n_spans = HOIST ? 1 : P.n_spans;
+  for (int k = 0; k < n_spans; ++k) {
     const double* T = P.log2rho + k * P.span_stride;
     const double* ca = T + oa;
     const double* cb = T + ob;
@@ -183,81 +188,79 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
     const double* hl = P.hl2 + (static_cast<size_t>(probe) * P.n_spans + k) * NS + sl;
     const bool fast = fabs(phi) * __ldg(P.wlast + k) > 1e-4;
     if (fast) {
-      const double* ze = P.zedge + static_cast<size_t>(k) * (NS + 1) + 1 + sl;
-      const bool l15 = sl == 15;
-      double pp = 0.0, pc = 0.0, ps = 0.0;  // previous block's (p, E): lane 15 defers
-      double c0v = 1.0, s0v = 0.0;          // E(z_0) of this span (1 for the first)
-      if (k > 0) dev_sincos(phi * __ldg(ze - 1 - sl), &c0v, &s0v);
-      // one step block ahead: the 8 loads of block b + 1 are in flight while
-      // block b computes (L1 hits ~35 cycles, the ~22 % L2 hits ~300)
-      double l0 = __ldg(ca), l1 = __ldg(ca + NS), l2 = __ldg(cb), l3 = __ldg(cb + NS);
-      double l4 = __ldg(cc3), l5 = __ldg(cc3 + NS), lh = __ldg(hl), lz = __ldg(ze);
+      const double* ze = P.zedge + static_cast<size_t>(k) * NS + sl;
+      double p0 = 0.0, pp = 0.0, pc = 0.0, ps = 0.0;
 #pragma unroll
       for (int b = 0; b < K; ++b) {
-        double lg = fma(w0, l0, -lh);
-        lg = fma(w1, l1, lg);
-        lg = fma(w2, l2, lg);
-        lg = fma(w3, l3, lg);
-        lg = fma(w4, l4, lg);
-        lg = fma(w5, l5, lg);
-        double ang = phi * lz;
-        if (b + 1 < K) {
-          const int o = 16 * (b + 1);
-          l0 = __ldg(ca + o);
-          l1 = __ldg(ca + NS + o);
-          l2 = __ldg(cb + o);
-          l3 = __ldg(cb + NS + o);
-          l4 = __ldg(cc3 + o);
-          l5 = __ldg(cc3 + NS + o);
-          lh = __ldg(hl + o);
-          lz = __ldg(ze + o);
-        }
+        const int o = 16 * b;
+        const double H = HOIST ? Hr[b] : __ldg(hl + o);
+        const double Z = HOIST ? Zr[b] : __ldg(ze + o);
+        double lg = fma(w0, __ldg(ca + o), -H);
+        lg = fma(w1, __ldg(ca + NS + o), lg);
+        lg = fma(w2, __ldg(cb + o), lg);
+        lg = fma(w3, __ldg(cb + NS + o), lg);
+        lg = fma(w4, __ldg(cc3 + o), lg);
+        lg = fma(w5, __ldg(cc3 + NS + o), lg);
         double p = dev_exp2_16(lg);
+        double ang = phi * Z;
         if (!FULL) {
-          const bool ok = sl + 16 * b < N;
+          const bool ok = sl * K + b < N;
           p = ok ? p : 0.0;
           ang = ok ? ang : 0.0;
         }
-        if (b == 0 && sl == 0) {  // -p_0 E(z_0)
-          fre = fma(-p, c0v, fre);
-          fim = fma(-p, s0v, fim);
-        }
         double cs, sn;
         dev_sincos(ang, &cs, &sn);
-        const double pr = __shfl_sync(segmask, p, rot, 16);
-        // lanes 0..14: (p_m - p_{m+1}) E_{m+1}; lane 15: the previous block's step
-        const double cf = (l15 ? pp : p) - pr;
-        fre = fma(cf, l15 ? pc : cs, fre);
-        fim = fma(cf, l15 ? ps : sn, fim);
+        if (b == 0) {
+          p0 = p;
+        } else {  // (p_{m-1} - p_m) E_m, E_m = end edge of the previous step
+          const double cf = pp - p;
+          fre = fma(cf, pc, fre);
+          fim = fma(cf, ps, fim);
+        }
         pp = p;
         pc = cs;
         ps = sn;
       }
-      if (l15) {  // p_N = 0
-        fre = fma(pp, pc, fre);
-        fim = fma(pp, ps, fim);
+      // the lane's last step pairs with the next lane's first (p_N = 0)
+      double pn = __shfl_down_sync(segmask, p0, 1, 16);
+      if (sl == 15) pn = 0.0;
+      const double cf = pp - pn;
+      fre = fma(cf, pc, fre);
+      fim = fma(cf, ps, fim);
+      // -p_0 E(z_0): E = 1 when the span starts at z = 0
+      const double z0 = __ldg(P.zstart + k);
+      if (z0 == 0.0) {
+        if (sl == 0) fre -= p0;
+      } else {
+        double c0v, s0v;
+        dev_sincos(phi * z0, &c0v, &s0v);
+        if (sl == 0) {
+          fre = fma(-p0, c0v, fre);
+          fim = fma(-p0, s0v, fim);
+        }
       }
     } else {
       const double* zm = P.zmid + static_cast<size_t>(k) * NS + sl;
       const double* wd = P.width + static_cast<size_t>(k) * NS + sl;
 #pragma unroll 1
       for (int b = 0; b < K; ++b) {
-        if (sl + 16 * b < N) {
-          double lg = fma(w0, __ldg(ca + 16 * b), -__ldg(hl + 16 * b));
-          lg = fma(w1, __ldg(ca + NS + 16 * b), lg);
-          lg = fma(w2, __ldg(cb + 16 * b), lg);
-          lg = fma(w3, __ldg(cb + NS + 16 * b), lg);
-          lg = fma(w4, __ldg(cc3 + 16 * b), lg);
-          lg = fma(w5, __ldg(cc3 + NS + 16 * b), lg);
+        if (FULL || sl * K + b < N) {
+          const int o = 16 * b;
+          double lg = fma(w0, __ldg(ca + o), -__ldg(hl + o));
+          lg = fma(w1, __ldg(ca + NS + o), lg);
+          lg = fma(w2, __ldg(cb + o), lg);
+          lg = fma(w3, __ldg(cb + NS + o), lg);
+          lg = fma(w4, __ldg(cc3 + o), lg);
+          lg = fma(w5, __ldg(cc3 + NS + o), lg);
           const double p = dev_exp2_16(lg);
-          const double wm = __ldg(wd + 16 * b);
+          const double wm = __ldg(wd + o);
           // sinc(x), |x| = |phi| w / 2 <= 5e-5 here: 1 - x^2/6 + x^4/120 is exact
           const double x = 0.5 * phi * wm;
           const double x2 = x * x;
           const double sinc = fma(x2, fma(x2, 1.0 / 120.0, -1.0 / 6.0), 1.0);
           const double w = p * wm * sinc;
           double cs, sn;
-          dev_sincos(phi * __ldg(zm + 16 * b), &cs, &sn);
+          dev_sincos(phi * __ldg(zm + o), &cs, &sn);
           sre = fma(w, cs, sre);
           sim = fma(w, sn, sim);
         }
@@ -276,7 +279,7 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
   return re * re + im * im;
 }
 
-template <int K, bool FULL>
+template <int K, bool FULL, bool HOIST>
 __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParams P) {
   __shared__ WarpSmem s_w[kWarps];
   if (threadIdx.x < 16) s_exp2_tab[threadIdx.x] = c_exp2_tab16[threadIdx.x];
@@ -290,6 +293,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
   const unsigned segmask = 0xffffu << (16 * seg);
   WarpSmem& S = s_w[warp];
   const int per_probe = P.n_q * P.n_r;
+  double Zr[K], Hr[K];
+  int cur_probe = -1;
+  if (HOIST) {
+#pragma unroll
+    for (int b = 0; b < K; ++b) Zr[b] = __ldg(P.zedge + 16 * b + sl);
+  }
 
   for (;;) {
     int row = 0;
@@ -297,6 +306,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
     row = __shfl_sync(kFull, row, 0);
     if (row >= P.total_rows) break;
     const int probe = row / per_probe;
+    if (HOIST && probe != cur_probe) {
+      cur_probe = probe;
+#pragma unroll
+      for (int b = 0; b < K; ++b) Hr[b] = __ldg(P.hl2 + static_cast<size_t>(probe) * NS + 16 * b + sl);
+    }
     const int n_r = P.n_r;
     double du1;
     {
@@ -403,7 +417,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
       const int n_act = __popc(am);
       n_eval += n_act;
       for (int idx = seg; idx < n_act; idx += 2) {
-        const double kv = point_kernel<K, FULL>(P, S, idx, probe, sl, segmask);
+        const double kv = point_kernel<K, FULL, HOIST>(P, S, idx, probe, sl, segmask, Zr, Hr);
         if (sl == 0) S.val[S.src[idx]] = S.pw[idx] * kv;
       }
       __syncwarp();
@@ -490,28 +504,31 @@ __global__ void finalize_channels_kernel(const FinalizeParams F) {
 using RowKernel = void (*)(const NliParams);
 
 template <int K>
-RowKernel pick(int steps) {
-  return steps == 16 * K ? nli_rows_kernel<K, true> : nli_rows_kernel<K, false>;
+RowKernel pick(int steps, bool one_span) {
+  constexpr bool kHoist = K <= 8;
+  if (one_span && kHoist)
+    return steps == 16 * K ? nli_rows_kernel<K, true, kHoist> : nli_rows_kernel<K, false, kHoist>;
+  return steps == 16 * K ? nli_rows_kernel<K, true, false> : nli_rows_kernel<K, false, false>;
 }
 
-RowKernel row_kernel_for(int steps) {
+RowKernel row_kernel_for(int steps, bool one_span) {
   switch ((steps + 15) / 16) {
-    case 1: return pick<1>(steps);
-    case 2: return pick<2>(steps);
-    case 3: return pick<3>(steps);
-    case 4: return pick<4>(steps);
-    case 5: return pick<5>(steps);
-    case 6: return pick<6>(steps);
-    case 7: return pick<7>(steps);
-    case 8: return pick<8>(steps);
-    case 9: return pick<9>(steps);
-    case 10: return pick<10>(steps);
-    case 11: return pick<11>(steps);
-    case 12: return pick<12>(steps);
-    case 13: return pick<13>(steps);
-    case 14: return pick<14>(steps);
-    case 15: return pick<15>(steps);
-    case 16: return pick<16>(steps);
+    case 1: return pick<1>(steps, one_span);
+    case 2: return pick<2>(steps, one_span);
+    case 3: return pick<3>(steps, one_span);
+    case 4: return pick<4>(steps, one_span);
+    case 5: return pick<5>(steps, one_span);
+    case 6: return pick<6>(steps, one_span);
+    case 7: return pick<7>(steps, one_span);
+    case 8: return pick<8>(steps, one_span);
+    case 9: return pick<9>(steps, one_span);
+    case 10: return pick<10>(steps, one_span);
+    case 11: return pick<11>(steps, one_span);
+    case 12: return pick<12>(steps, one_span);
+    case 13: return pick<13>(steps, one_span);
+    case 14: return pick<14>(steps, one_span);
+    case 15: return pick<15>(steps, one_span);
+    case 16: return pick<16>(steps, one_span);
     default: return nullptr;
   }
 }
@@ -564,8 +581,8 @@ int launch_finalize_channels_only(const FinalizeParams& f, cudaStream_t st) {
   return 1;
 }
 
-int nli_ctas_per_sm(int steps) {
-  RowKernel k = row_kernel_for(steps);
+int nli_ctas_per_sm(int steps, bool one_span) {
+  RowKernel k = row_kernel_for(steps, one_span);
   if (!k) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kWarps * 32, 0) != cudaSuccess) return 0;
@@ -574,7 +591,12 @@ int nli_ctas_per_sm(int steps) {
 
 int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaStream_t stream,
                cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
-  RowKernel k = row_kernel_for(p.steps);
+  // UWB_NLI_NO_HOIST=1 selects the per-point z/half-log loads (A/B experiments)
+  static const bool no_hoist = [] {
+    const char* e = std::getenv("UWB_NLI_NO_HOIST");
+    return e && e[0] == '1';
+  }();
+  RowKernel k = row_kernel_for(p.steps, p.n_spans == 1 && !no_hoist);
   if (!k || p.n_probes <= 0 || p.col_stride != 16 * ((p.steps + 15) / 16)) return -1;
   int launches = 0;
   cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), stream);

@@ -4,9 +4,17 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <vector>
 
 namespace uwb {
+
+// Lane order of the distance steps.  A column of NS = 16 K
+// doubles holds step m at position (m % K) * 16 + m / K: lane sl of a 16-lane
+// segment owns the K consecutive steps m = sl K + b, b = 0..K-1, and for a
+// fixed b the 16 lanes read 16 consecutive doubles (one 128-byte line).
+__host__ __device__ __forceinline__ int lane_pos(int m, int K) { return (m % K) * 16 + m / K; }
 
 // Everything the integrand kernel reads.  All pointers are device memory.
 struct NliParams {
@@ -15,15 +23,17 @@ struct NliParams {
   const double* freq;
   const double* psd;
   double spacing, bch, centre, half_band;
-  // Spans: log2(rho) tables [span][ch][m] (reference layout ch*steps+m, scaled
-  // by log2 e so the integrand can use exp2), span-absolute edge/mid, widths.
+  // Spans: log2(rho) tables [span][ch][lane_pos(m)] (the reference's log_rho
+  // ch*steps+m scaled by log2 e so the integrand can use exp2), span-absolute
+  // step geometry, all in lane order.
   int n_spans;
   int steps;
   int col_stride;         // NS = 16 * ceil(steps / 16): padded column length (doubles)
   const double* log2rho;  // [n_spans][n_ch + 1][NS]: log2 rho, zero pad column n and pad steps
   size_t span_stride;     // (n_ch + 1) * NS, or 0 when every span shares one table
-  const double* zedge;    // [n_spans][NS + 1] = z_base + edge (edges past N repeat L)
-  const double* zmid;     // [n_spans][NS]     = z_base + mid
+  const double* zedge;    // [n_spans][NS] z_base + edge[m + 1] (pad steps repeat the span end)
+  const double* zstart;   // [n_spans]     z_base + edge[0]
+  const double* zmid;     // [n_spans][NS] z_base + mid[m]
   const double* width;    // [n_spans][NS]
   const double* wlast;    // [n_spans] width.back(): fast/slow switch (gn_integral.hpp:156)
   double beta2, beta3, beta4;
@@ -63,6 +73,29 @@ struct FinalizeParams {
   uint8_t* skipped;  // [n_ch]
 };
 
+// Host: append one span's lane-ordered geometry (the NliParams zedge / zstart /
+// zmid / width / wlast arrays) for a span starting at z_base.
+struct SpanTables {
+  std::vector<double> zend, zstart, zmid, width, wlast;
+};
+inline void append_span_tables(const double* edge, const double* mid, const double* width,
+                               int steps, double z_base, SpanTables* t) {
+  const int K = (steps + 15) / 16, NS = 16 * K;
+  const size_t o = t->zend.size();
+  t->zend.resize(o + NS);
+  t->zmid.resize(o + NS);
+  t->width.resize(o + NS);
+  for (int m = 0; m < NS; ++m) {
+    const int e = lane_pos(m, K);
+    const int mm = std::min(m, steps - 1);
+    t->zend[o + e] = z_base + edge[std::min(m + 1, steps)];
+    t->zmid[o + e] = z_base + mid[mm];
+    t->width[o + e] = width[mm];
+  }
+  t->zstart.push_back(z_base + edge[0]);
+  t->wlast.push_back(width[steps - 1]);
+}
+
 // Issue the NLI pipeline on `stream`: queue reset, probe half-log columns,
 // integrand rows (persistent, grid_ctas CTAs), per-probe and per-channel
 // finalize.  ev_k0/ev_k1 (may be null) bracket the integrand kernel.
@@ -71,7 +104,7 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
                cudaEvent_t ev_k0, cudaEvent_t ev_k1);
 
 // CTAs per SM the integrand kernel reaches for a given step count.
-int nli_ctas_per_sm(int steps);
+int nli_ctas_per_sm(int steps, bool one_span);
 constexpr int kMaxSteps = 256;  // 16 lanes x 16 steps per lane
 // Elements allocated past the end of log2rho / zedge / hl2: the integrand's
 // lanes with m >= N load them and mask the result (branch-free tail).

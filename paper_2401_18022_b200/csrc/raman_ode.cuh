@@ -5,6 +5,8 @@
 
 #include <cstddef>
 
+#include "nli_kernel.cuh"
+
 namespace uwb {
 
 constexpr int kMaxOdeChannels = 2560;  // 640 threads x 4 channels per thread
@@ -24,6 +26,7 @@ struct OdeParams {
   double seg_b[kMaxRamanSegments];
   int steps;             // distance-grid steps (midpoints)
   int col_stride;        // row stride of log2rho / log_rho (>= steps)
+  int lane_k;            // > 0: log2rho in the integrand's lane order lane_pos(m, lane_k)
   const double* mid;     // [steps]
   double length;
   double rtol, atol;

@@ -72,26 +72,24 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   const int NS = 16 * ((steps + 15) / 16);
   const size_t cols = static_cast<size_t>(n + 1) * NS;
   std::vector<double> tab(static_cast<size_t>(n_spans) * cols, 0.0);
-  std::vector<double> ze(static_cast<size_t>(n_spans) * (NS + 1));
-  std::vector<double> zm(static_cast<size_t>(n_spans) * NS);
-  std::vector<double> wd(static_cast<size_t>(n_spans) * NS);
-  std::vector<double> wl(n_spans);
+  SpanTables stb;
+  const int K = NS / 16;
   double z_base = 0.0;
   for (int k = 0; k < n_spans; ++k) {
     const uwb_span& s = spans[k];
     double* t = tab.data() + static_cast<size_t>(k) * cols;
     for (int ch = 0; ch < n; ++ch)
       for (int m = 0; m < steps; ++m)
-        t[static_cast<size_t>(ch) * NS + m] = s.log_rho[static_cast<size_t>(ch) * steps + m] * kLog2e;
-    for (int m = 0; m <= NS; ++m)
-      ze[static_cast<size_t>(k) * (NS + 1) + m] = z_base + s.edge[std::min(m, steps)];
-    for (int m = 0; m < NS; ++m) {
-      zm[static_cast<size_t>(k) * NS + m] = z_base + s.mid[std::min(m, steps - 1)];
-      wd[static_cast<size_t>(k) * NS + m] = s.width[std::min(m, steps - 1)];
-    }
-    wl[k] = s.width[steps - 1];
+        t[static_cast<size_t>(ch) * NS + lane_pos(m, K)] =
+            s.log_rho[static_cast<size_t>(ch) * steps + m] * kLog2e;
+    append_span_tables(s.edge, s.mid, s.width, steps, z_base, &stb);
     z_base += s.length;
   }
+  const std::vector<double>& ze = stb.zend;
+  const std::vector<double>& zm = stb.zmid;
+  const std::vector<double>& wd = stb.width;
+  const std::vector<double>& wl = stb.wlast;
+  const std::vector<double>& zs = stb.zstart;
   double* d_freq = c->freq.get<double>(n);
   double* d_psd = c->psd.get<double>(n);
   double* d_tab = c->log2rho.get<double>(tab.size());
@@ -99,7 +97,8 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   double* d_zm = c->zmid.get<double>(zm.size());
   double* d_wd = c->width.get<double>(wd.size());
   double* d_wl = c->wlast.get<double>(wl.size());
-  if (!d_freq || !d_psd || !d_tab || !d_ze || !d_zm || !d_wd || !d_wl)
+  double* d_zs = c->zstart.get<double>(zs.size());
+  if (!d_freq || !d_psd || !d_tab || !d_ze || !d_zm || !d_wd || !d_wl || !d_zs)
     return fail(UWB_CUDA_ERROR, "device allocation failed");
   cudaStream_t st = c->stream;
   xfer(c, d_freq, g->freq, n * sizeof(double), cudaMemcpyHostToDevice, st);
@@ -109,6 +108,7 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   xfer(c, d_zm, zm.data(), zm.size() * sizeof(double), cudaMemcpyHostToDevice, st);
   xfer(c, d_wd, wd.data(), wd.size() * sizeof(double), cudaMemcpyHostToDevice, st);
   xfer(c, d_wl, wl.data(), wl.size() * sizeof(double), cudaMemcpyHostToDevice, st);
+  xfer(c, d_zs, zs.data(), zs.size() * sizeof(double), cudaMemcpyHostToDevice, st);
   // the vectors die at return: make the copies complete first
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "upload");
@@ -126,6 +126,7 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   P->col_stride = NS;
   P->span_stride = cols;
   P->zedge = d_ze;
+  P->zstart = d_zs;
   P->zmid = d_zm;
   P->width = d_wd;
   P->wlast = d_wl;
@@ -203,7 +204,7 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
   }
   cudaEventRecord(c->ev0, st);
   if (np) {
-    const int per_sm = nli_ctas_per_sm(P.steps);
+    const int per_sm = nli_ctas_per_sm(P.steps, P.n_spans == 1);
     if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
     const int launched = launch_nli(P, F, c->sm_count * per_sm, st, c->evk0, c->evk1);
     if (launched < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
@@ -294,7 +295,7 @@ int uwb_ctx_create(int device, uwb_ctx** out) {
   cudaEventCreate(&c->evk0);
   cudaEventCreate(&c->evk1);
   // probe the kernel image: fails loudly if the fatbin has no sm_100a code
-  if (nli_ctas_per_sm(112) <= 0) {
+  if (nli_ctas_per_sm(112, true) <= 0) {
     uwb_ctx_destroy(c);
     return set_err(UWB_CUDA_ERROR, "integrand kernel not loadable on this device");
   }
@@ -307,7 +308,7 @@ void uwb_ctx_destroy(uwb_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   release_link_state(c);
-  for (DBuf* b : {&c->freq, &c->psd, &c->gamma, &c->log2rho, &c->zedge, &c->zmid, &c->width,
+  for (DBuf* b : {&c->freq, &c->psd, &c->gamma, &c->log2rho, &c->zedge, &c->zstart, &c->zmid, &c->width,
                   &c->wlast, &c->probe_nu, &c->probe_gamma, &c->hl2, &c->rowsum, &c->counter,
                   &c->n_eval, &c->probe_g, &c->probe_quad, &c->chan_probe0, &c->eta, &c->nli_psd,
                   &c->nli_power, &c->quad, &c->skipped, &c->alpha, &c->aeff, &c->raman_x,

@@ -55,7 +55,7 @@ struct uwb_ctx {
   // channel grid
   uwb::DBuf freq, psd, gamma;
   // spans
-  uwb::DBuf log2rho, zedge, zmid, width, wlast;
+  uwb::DBuf log2rho, zedge, zstart, zmid, width, wlast;
   // probes + work
   uwb::DBuf probe_nu, probe_gamma, hl2, rowsum, counter, n_eval, probe_g, probe_quad, chan_probe0;
   // per-channel results

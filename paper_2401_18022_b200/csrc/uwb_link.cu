@@ -231,15 +231,10 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   // span-absolute grids: every span is a copy of the one evolution
   // (solve_link_noise :185); padded layout of nli_kernel.cuh
   const int NS = 16 * ((steps + 15) / 16);
-  std::vector<double> ze, zm, wd, wl;
+  SpanTables st;
   double z_base = 0.0;
   for (int k = 0; k < fb->span_count; ++k) {
-    for (int m = 0; m <= NS; ++m) ze.push_back(z_base + edge[std::min(m, steps)]);
-    for (int m = 0; m < NS; ++m) {
-      zm.push_back(z_base + mid[std::min(m, steps - 1)]);
-      wd.push_back(width[std::min(m, steps - 1)]);
-    }
-    wl.push_back(width[steps - 1]);
+    append_span_tables(edge.data(), mid.data(), width.data(), steps, z_base, &st);
     z_base += fb->length_m;
   }
   P.n_ch = n;
@@ -256,10 +251,11 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   cudaMemsetAsync(const_cast<double*>(P.log2rho), 0, cols * sizeof(double), c->stream);  // pads
   P.col_stride = NS;
   P.span_stride = 0;
-  P.zedge = up(c, c->zedge, ze.data(), ze.size());
-  P.zmid = up(c, c->zmid, zm.data(), zm.size());
-  P.width = up(c, c->width, wd.data(), wd.size());
-  P.wlast = up(c, c->wlast, wl.data(), wl.size());
+  P.zedge = up(c, c->zedge, st.zend.data(), st.zend.size());
+  P.zstart = up(c, c->zstart, st.zstart.data(), st.zstart.size());
+  P.zmid = up(c, c->zmid, st.zmid.data(), st.zmid.size());
+  P.width = up(c, c->width, st.width.data(), st.width.size());
+  P.wlast = up(c, c->wlast, st.wlast.data(), st.wlast.size());
   P.beta2 = fb->beta[0];
   P.beta3 = fb->beta[1];
   P.beta4 = fb->beta[2];
@@ -319,6 +315,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   double* d_tmp = w + 5 * n + 2;
   O.steps = steps;
   O.col_stride = NS;
+  O.lane_k = NS / 16;
   O.mid = d_mid;
   O.length = fb->length_m;
   O.rtol = pr->rtol;
@@ -348,7 +345,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   L.out = c->report.get<double>(4 * static_cast<size_t>(n) + 3 + 2 * L.n_bands);
   L.tmp = d_tmp;
 
-  const int per_sm = nli_ctas_per_sm(steps);
+  const int per_sm = nli_ctas_per_sm(steps, P.n_spans == 1);
   if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
   pr->grid_ctas = c->sm_count * per_sm;
   cudaError_t e = cudaStreamSynchronize(c->stream);
@@ -566,6 +563,7 @@ int uwb_power_evolution(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre
   O.coef_v = O.coef_u + n;
   O.steps = steps;
   O.col_stride = steps;
+  O.lane_k = 0;
   O.mid = d_mid;
   O.length = fibre->length_m;
   O.rtol = link->rtol > 0 ? link->rtol : 1e-9;

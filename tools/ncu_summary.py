@@ -33,7 +33,7 @@ for k in keys:
     if k in m:
         print(f"{k:80s} {m[k]}")
 stalls = {k: float(v2) for k, v2 in m.items()
-          if k.startswith("smsp__average_warp_latency_issue_stalled") and k.endswith(".ratio")
+          if k.startswith("smsp__average_warps_issue_stalled") and k.endswith("per_issue_active.ratio")
           and v2 not in ("", "n/a")}
 if not stalls:
     stalls = {k: float(v2) for k, v2 in m.items()
