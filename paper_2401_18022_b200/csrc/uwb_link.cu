@@ -78,26 +78,52 @@ __global__ void link_channels_kernel(LinkDev L) {
   L.tmp[2 * L.n + i] = l2;
 }
 
-// Ordered sums (loss, capacity, powers) in channel order (:224-235).
-__global__ void link_totals_kernel(LinkDev L) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double loss = 0.0, cap = 0.0, total_w = 0.0;
-  double* bp = L.out + 4 * L.n + 3;
-  double* bc = bp + L.n_bands;
-  for (int b = 0; b < L.n_bands; ++b) bp[b] = bc[b] = 0.0;
-  for (int i = 0; i < L.n; ++i) {
-    const double p = L.tmp[i];
-    if (p < 0.0) continue;
-    loss -= L.tmp[2 * L.n + i];
-    cap += L.tmp[L.n + i];
-    total_w += p;
-    const int b = L.band ? L.band[i] : -1;
-    if (b >= 0 && b < L.n_bands) {
-      bp[b] += p;
-      bc[b] += L.tmp[L.n + i];
-    }
+// Ordered sums (loss, capacity, powers) in channel order (:224-235).  The
+// block stages the per-channel terms in shared memory, then one thread runs
+// the reference's sequential sums out of shared memory (the order is part of
+// the result; a global-memory loop costs a dependent L2 round trip per channel).
+constexpr int kTotalsThreads = 256;
+constexpr int kMaxBands = 16;
+
+__global__ void __launch_bounds__(kTotalsThreads) link_totals_kernel(LinkDev L) {
+  extern __shared__ double sm_tot[];
+  double* sp = sm_tot;           // [n] p (< 0: inactive)
+  double* sc = sp + L.n;         // [n] capacity
+  double* sl = sc + L.n;         // [n] log2(1 + snr)
+  int* sb = reinterpret_cast<int*>(sl + L.n);  // [n] band
+  for (int i = threadIdx.x; i < L.n; i += blockDim.x) {
+    sp[i] = L.tmp[i];
+    sc[i] = L.tmp[L.n + i];
+    sl[i] = L.tmp[2 * L.n + i];
+    sb[i] = L.band ? L.band[i] : -1;
   }
-  for (int b = 0; b < L.n_bands; ++b) bp[b] = bp[b] > 0.0 ? 10.0 * log10(bp[b] / 1e-3) : -300.0;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const int nb = L.n_bands < kMaxBands ? L.n_bands : kMaxBands;
+  double bp[kMaxBands], bc[kMaxBands];
+#pragma unroll
+  for (int b = 0; b < kMaxBands; ++b) bp[b] = bc[b] = 0.0;
+  double loss = 0.0, cap = 0.0, total_w = 0.0;
+  for (int i = 0; i < L.n; ++i) {
+    const double p = sp[i];
+    if (p < 0.0) continue;
+    loss -= sl[i];
+    cap += sc[i];
+    total_w += p;
+    const int b = sb[i];
+#pragma unroll
+    for (int k = 0; k < kMaxBands; ++k)
+      if (k == b && k < nb) {
+        bp[k] += p;
+        bc[k] += sc[i];
+      }
+  }
+  double* op = L.out + 4 * L.n + 3;
+  double* oc = op + L.n_bands;
+  for (int b = 0; b < L.n_bands; ++b) {
+    op[b] = b < nb && bp[b] > 0.0 ? 10.0 * log10(bp[b] / 1e-3) : -300.0;
+    oc[b] = b < nb ? bc[b] : 0.0;
+  }
   L.out[4 * L.n + 0] = loss;
   L.out[4 * L.n + 1] = cap;
   L.out[4 * L.n + 2] = total_w > 0.0 ? 10.0 * log10(total_w / 1e-3) : -300.0;
@@ -338,6 +364,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   L.rho_end = d_rho_end;
   L.nf_db = d_nf;
   L.band = d_band2;
+  if (lk->n_bands > kMaxBands) return fail(UWB_CONFIG_ERROR, "uwb: at most 16 bands");
   L.n_bands = std::max(lk->n_bands, 0);
   L.span_count = fb->span_count;
   L.use_snr_trx = lk->use_snr_trx;
@@ -386,7 +413,12 @@ int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st) {
 int run_report(uwb_ctx* c, cudaStream_t st) {
   LinkDev L = c->prep->L;
   link_channels_kernel<<<(L.n + 127) / 128, 128, 0, st>>>(L);
-  link_totals_kernel<<<1, 32, 0, st>>>(L);
+  const size_t smem = static_cast<size_t>(L.n) * (3 * sizeof(double) + sizeof(int));
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      link_totals_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      static_cast<int>(kMaxOdeChannels * (3 * sizeof(double) + sizeof(int))));
+  (void)attr;
+  link_totals_kernel<<<1, kTotalsThreads, smem, st>>>(L);
   c->last_launches += 2;
   cudaEventRecord(c->ev1, st);
   cudaError_t e = cudaGetLastError();

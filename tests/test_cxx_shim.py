@@ -1,0 +1,32 @@
+"""The C++ drop-in (include/uwblink_b200/gn_integral.hpp) run as a reference
+user would: tests/cxx/shim_parity.cpp is compiled against the UNMODIFIED
+reference headers (oracle/Makefile `shim`, in the container that has
+/root/reference) and restates the reference's own Catch2 assertions with
+uwblink::b200::* in place of uwblink::*, comparing with the reference's CPU
+result on the same inputs.  The binary travels to the GPU box prebuilt."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "oracle", "_ref", "shim_parity")
+
+
+def test_shim_header_is_self_contained():
+    """The shim only needs uwb_nli.h + the reference headers (no torch, no
+    Python): check the include list without compiling."""
+    src = open(os.path.join(ROOT, "include", "uwblink_b200", "gn_integral.hpp")).read()
+    incs = [l.split()[1] for l in src.splitlines() if l.startswith("#include")]
+    assert '"uwb_nli.h"' in incs and '"uwblink/gn_integral.hpp"' in incs
+    assert not any("torch" in i or "cuda" in i for i in incs)
+
+
+@pytest.mark.gpu
+def test_cxx_shim_parity():
+    if not os.path.exists(BIN):
+        pytest.skip("oracle/_ref/shim_parity not built (needs /root/reference at build time)")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failure(s)" in r.stdout
