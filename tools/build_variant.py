@@ -1,0 +1,23 @@
+"""Build an A/B variant of libuwbnli.so with extra -D flags into scratch/v/.
+
+    python tools/build_variant.py NAME [-DFOO=1 ...]
+Load it with UWB_LIB_PATH=scratch/v/NAME.so (paper_2401_18022_b200/_native.py).
+"""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2401_18022_b200 import build as b  # noqa: E402
+
+name, defs = sys.argv[1], sys.argv[2:]
+out_dir = os.path.join(ROOT, "scratch", "v")
+os.makedirs(out_dir, exist_ok=True)
+out = os.path.join(out_dir, name + ".so")
+cmd = [b.nvcc()] + b.ARCH + b.FLAGS + defs + ["-o", out] + [os.path.join(b.CSRC, s) for s in b.SOURCES]
+r = subprocess.run(cmd, capture_output=True, text=True)
+if r.returncode:
+    sys.stderr.write(r.stdout + r.stderr)
+    sys.exit(1)
+print(out)

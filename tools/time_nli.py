@@ -1,0 +1,50 @@
+"""A/B timing of the integrand: median device time of nli_rows over R full
+evaluations of the bench workload, plus an eta checksum (variants must agree).
+
+    UWB_LIB_PATH=scratch/v/x.so python tools/time_nli.py [--n-r 150] [--density 1.4] [--reps 7]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2401_18022_b200 as uwb  # noqa: E402
+
+p = argparse.ArgumentParser()
+p.add_argument("--n-r", type=int, default=150)
+p.add_argument("--density", type=float, default=1.4)
+p.add_argument("--reps", type=int, default=7)
+p.add_argument("--tag", default=os.environ.get("UWB_LIB_PATH", "main"))
+a = p.parse_args()
+eng = uwb.Engine(0)
+grid = uwb.make_default_uwb_grid()
+uwb.set_uniform_launch(grid, 1e-3)
+res = uwb.ResidentLink(uwb.default_fibre(), grid,
+                       uwb.LinkConfig(gn=uwb.GnSolverConfig(n_r=a.n_r, mean_step_density=a.density)),
+                       engine=eng)
+st = torch.cuda.Stream()
+torch.cuda.set_stream(st)
+psd = torch.tensor(grid.psd, dtype=torch.float64, device="cuda:0")
+rep = torch.zeros(res.report_len, dtype=torch.float64, device="cuda:0")
+ks, ts = [], []
+for i in range(a.reps + 2):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    res.run(psd.data_ptr(), rep.data_ptr(), st.cuda_stream)
+    e1.record(st)
+    torch.cuda.synchronize()
+    if i >= 2:
+        ks.append(eng.last_nli_stats()["kernel_ms"])
+        ts.append(e0.elapsed_time(e1))
+res.check_status()
+n = grid.size()
+eta = rep[:n].cpu().numpy()
+print(json.dumps({"tag": a.tag, "n_r": a.n_r, "density": a.density,
+                  "nli_ms": float(np.median(ks)), "eval_ms": float(np.median(ts)),
+                  "eta_sum": float(np.sum(eta)), "eta_max": float(np.max(eta)),
+                  "loss": float(rep[4 * n].item())}), flush=True)
