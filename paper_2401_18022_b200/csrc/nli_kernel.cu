@@ -40,7 +40,13 @@ namespace uwb {
 
 namespace {
 
-constexpr int kWarps = 8;  // warps per CTA
+#ifndef UWB_NLI_WARPS
+#define UWB_NLI_WARPS 8
+#endif
+#ifndef UWB_NLI_MIN_BLOCKS
+#define UWB_NLI_MIN_BLOCKS 2
+#endif
+constexpr int kWarps = UWB_NLI_WARPS;  // warps per CTA
 constexpr unsigned kFull = 0xffffffffu;
 
 __constant__ double c_exp2_tab16[16] = UWB_EXP2_TABLE16;
@@ -279,110 +285,8 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
   return re * re + im * im;
 }
 
-#ifndef UWB_NLI_ILP2
-#define UWB_NLI_ILP2 0
-#endif
-#ifndef UWB_NLI_ILP2_HOIST
-#define UWB_NLI_ILP2_HOIST 0
-#endif
-
-// Two FAST points per 16-lane segment, single span, steps interleaved: the
-// two points share the lane's z / half-log operands and give every lane two
-// independent exp/sincos chains per step (latency hiding at 4 warps/SMSP).
 template <int K, bool FULL, bool HOIST>
-__device__ __forceinline__ void point_kernel2_fast(const NliParams& P, const WarpSmem& S, int ia,
-                                                   int ib, int probe, int sl, unsigned segmask,
-                                                   const double (&Zr)[K], const double (&Hr)[K],
-                                                   double* out_a, double* out_b) {
-  constexpr int NS = 16 * K;
-  const int N = P.steps;
-  const double phA = S.phi[ia], phB = S.phi[ib];
-  const double a0 = S.w[0][ia], a1 = S.w[1][ia], a2 = S.w[2][ia], a3 = S.w[3][ia],
-               a4 = S.w[4][ia], a5 = S.w[5][ia];
-  const double b0 = S.w[0][ib], b1 = S.w[1][ib], b2 = S.w[2][ib], b3 = S.w[3][ib],
-               b4 = S.w[4][ib], b5 = S.w[5][ib];
-  const double* T = P.log2rho;
-  const double* A0 = T + S.col[0][ia] + sl;
-  const double* A1 = T + S.col[1][ia] + sl;
-  const double* A2 = T + S.col[2][ia] + sl;
-  const double* B0 = T + S.col[0][ib] + sl;
-  const double* B1 = T + S.col[1][ib] + sl;
-  const double* B2 = T + S.col[2][ib] + sl;
-  const double* hl = P.hl2 + static_cast<size_t>(probe) * NS + sl;
-  const double* ze = P.zedge + sl;
-  double fa = 0.0, ga = 0.0, fb = 0.0, gb = 0.0;  // (re, im) of the fast sums
-  double pa0 = 0.0, ppa = 0.0, pca = 0.0, psa = 0.0;
-  double pb0 = 0.0, ppb = 0.0, pcb = 0.0, psb = 0.0;
-#pragma unroll
-  for (int b = 0; b < K; ++b) {
-    const int o = 16 * b;
-    const double H = HOIST ? Hr[b] : __ldg(hl + o);
-    const double Z = HOIST ? Zr[b] : __ldg(ze + o);
-    double la = fma(a0, __ldg(A0 + o), -H);
-    double lb = fma(b0, __ldg(B0 + o), -H);
-    la = fma(a1, __ldg(A0 + NS + o), la);
-    lb = fma(b1, __ldg(B0 + NS + o), lb);
-    la = fma(a2, __ldg(A1 + o), la);
-    lb = fma(b2, __ldg(B1 + o), lb);
-    la = fma(a3, __ldg(A1 + NS + o), la);
-    lb = fma(b3, __ldg(B1 + NS + o), lb);
-    la = fma(a4, __ldg(A2 + o), la);
-    lb = fma(b4, __ldg(B2 + o), lb);
-    la = fma(a5, __ldg(A2 + NS + o), la);
-    lb = fma(b5, __ldg(B2 + NS + o), lb);
-    double pa = dev_exp2_16(la);
-    double pb = dev_exp2_16(lb);
-    double anga = phA * Z, angb = phB * Z;
-    if (!FULL) {
-      const bool ok = sl * K + b < N;
-      pa = ok ? pa : 0.0;
-      pb = ok ? pb : 0.0;
-      anga = ok ? anga : 0.0;
-      angb = ok ? angb : 0.0;
-    }
-    double ca, sa, cb, sb;
-    dev_sincos(anga, &ca, &sa);
-    dev_sincos(angb, &cb, &sb);
-    if (b == 0) {
-      pa0 = pa;
-      pb0 = pb;
-    } else {
-      const double cfa = ppa - pa, cfb = ppb - pb;
-      fa = fma(cfa, pca, fa);
-      ga = fma(cfa, psa, ga);
-      fb = fma(cfb, pcb, fb);
-      gb = fma(cfb, psb, gb);
-    }
-    ppa = pa; pca = ca; psa = sa;
-    ppb = pb; pcb = cb; psb = sb;
-  }
-  double pna = __shfl_down_sync(segmask, pa0, 1, 16);
-  double pnb = __shfl_down_sync(segmask, pb0, 1, 16);
-  if (sl == 15) pna = pnb = 0.0;
-  fa = fma(ppa - pna, pca, fa);
-  ga = fma(ppa - pna, psa, ga);
-  fb = fma(ppb - pnb, pcb, fb);
-  gb = fma(ppb - pnb, psb, gb);
-  if (sl == 0) {  // span 0 starts at z = 0 (checked by the caller): -p_0 E(0) = -p_0
-    fa -= pa0;
-    fb -= pb0;
-  }
-  const double ia_ = S.invphi[ia], ib_ = S.invphi[ib];
-  double rea = ga * ia_, ima = -fa * ia_;
-  double reb = gb * ib_, imb = -fb * ib_;
-#pragma unroll
-  for (int o = 8; o >= 1; o >>= 1) {
-    rea += __shfl_xor_sync(segmask, rea, o, 16);
-    ima += __shfl_xor_sync(segmask, ima, o, 16);
-    reb += __shfl_xor_sync(segmask, reb, o, 16);
-    imb += __shfl_xor_sync(segmask, imb, o, 16);
-  }
-  *out_a = rea * rea + ima * ima;
-  *out_b = reb * reb + imb * imb;
-}
-
-template <int K, bool FULL, bool HOIST>
-__global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParams P) {
+__global__ void __launch_bounds__(kWarps * 32, UWB_NLI_MIN_BLOCKS) nli_rows_kernel(const NliParams P) {
   __shared__ WarpSmem s_w[kWarps];
   if (threadIdx.x < 16) s_exp2_tab[threadIdx.x] = c_exp2_tab16[threadIdx.x];
   __syncthreads();
@@ -519,22 +423,6 @@ __global__ void __launch_bounds__(kWarps * 32, 2) nli_rows_kernel(const NliParam
       const int n_act = __popc(am);
       n_eval += n_act;
       int base = 0;
-#if UWB_NLI_ILP2
-      // pairs of fast points per segment (fast points are listed first); the
-      // span must start at z = 0 (-p_0 E_0 = -p_0), else the single-point path
-      if (P.n_spans == 1 && __ldg(P.zstart) == 0.0) {
-        const int n_fast = __popc(fm);
-        for (; base + 4 <= n_fast; base += 4) {
-          double ka, kb;
-          point_kernel2_fast<K, FULL, HOIST && UWB_NLI_ILP2_HOIST>(
-              P, S, base + seg, base + 2 + seg, probe, sl, segmask, Zr, Hr, &ka, &kb);
-          if (sl == 0) {
-            S.val[S.src[base + seg]] = S.pw[base + seg] * ka;
-            S.val[S.src[base + 2 + seg]] = S.pw[base + 2 + seg] * kb;
-          }
-        }
-      }
-#endif
       // warp-uniform trip count: with an odd count the idle half-warp repeats
       // its partner's point (same branch, result dropped) instead of diverging
       for (; base < n_act; base += 2) {
