@@ -9,7 +9,7 @@
 
 namespace uwb {
 
-constexpr int kMaxOdeChannels = 2560;  // 640 threads x 4 channels per thread
+constexpr int kMaxOdeChannels = 2560;  // 512 threads x 5 channels per thread
 constexpr int kMaxRamanSegments = 4;  // linear pieces of the gain table in d = |j - i|
 
 struct OdeParams {
