@@ -94,13 +94,19 @@ __device__ __forceinline__ double phase_mismatch(double f1, double f2, double fi
 // Per-warp shared state for one chunk of 32 u2 columns, plus the row's
 // parameters (parked here so they are not live in registers across the
 // integrand loop).
+// One listed point, packed so a 16-lane segment reads it with five broadcast
+// 128-bit loads.
+struct alignas(16) PointRec {
+  double w[6];        // 16 x half weights for columns i0 and i0 + 1 of nu1, nu2, nu3
+  double phi, invphi;  // invphi = 1/phi (0 when phi == 0: no fast span then)
+  int col[3];          // element offset (i0 * NS) of each stencil's first column
+  int src;             // chunk-local column of the listed point
+  double pw;           // p1 * p2 * p3
+  double pad;
+};
+
 struct WarpSmem {
-  int col[3][32];    // element offset (i0 * NS) of each stencil's first column
-  double w[6][32];   // 16 x half weights for columns i0 and i0 + 1 of nu1, nu2, nu3
-  double phi[32];
-  double invphi[32];  // 1/phi (0 when phi == 0: no fast span then)
-  double pw[32];     // p1 * p2 * p3
-  int src[32];       // chunk-local column of the listed point
+  PointRec pt[32];
   double val[32];    // pw * |kernel|^2 per chunk column
   double nu, f, s1, s2, su, u1, lo, du2, row_acc;
 };
@@ -133,8 +139,12 @@ __device__ __forceinline__ double dev_exp2_16(double x) {
   return __hiloint2double(__double2hiint(s) + ((k >> 4) << 20), __double2loint(s));
 }
 
+#ifndef UWB_NLI_SINCOS_TABLE
+#define UWB_NLI_SINCOS_TABLE 1
+#endif
+
 // (cos x, sin x) for |x| < 2^50 (uwb_devmath.cuh sincos_rd): 18 FP64 instructions.
-__device__ __forceinline__ void dev_sincos(double x, double* c_out, double* s_out) {
+__device__ __forceinline__ void dev_sincos_quadrant(double x, double* c_out, double* s_out) {
   const double t = fma(x, c_red[0], kMagic);
   const int q = __double2loint(t);
   const double kd = t - kMagic;
@@ -161,6 +171,49 @@ __device__ __forceinline__ void dev_sincos(double x, double* c_out, double* s_ou
   *c_out = __hiloint2double(__double2hiint(co) ^ (((q + 1) & 2) << 30), __double2loint(co));
 }
 
+// (cos x, sin x) for |x| < 2^50 by a 16-entry full-circle table: x = k pi/8
+// + r, |r| <= pi/16, cos/sin(k pi/8) from two 128-byte shared tables (one
+// line each: conflict-free for any lane pattern), minimax kernels on r
+// (sin: r + r^3 S(r^2), deg 3, |err| 3.3e-18; cos: 1 + r^2 C(r^2), deg 4,
+// |err| 1.3e-20; Chebyshev fits in 50-digit arithmetic), then the angle
+// addition.  19 FP64 instructions and no quadrant selects / sign fix-ups.
+__constant__ double c_red8[3] = {kEightOverPi, -kPio8Hi, -kPio8Lo};
+__constant__ double c_s16[4] = {kS16c1, kS16c2, kS16c3, kS16c4};
+__constant__ double c_c16[5] = {kC16c0, kC16c1, kC16c2, kC16c3, kC16c4};
+__constant__ double c_tab_cos16[16] = UWB_COS_TABLE16;
+__constant__ double c_tab_sin16[16] = UWB_SIN_TABLE16;
+__shared__ double s_cos16[16];
+__shared__ double s_sin16[16];
+
+__device__ __forceinline__ void dev_sincos_table(double x, double* c_out, double* s_out) {
+  const double t = fma(x, c_red8[0], kMagic);
+  const int q = __double2loint(t) & 15;
+  const double kd = t - kMagic;
+  double r = fma(kd, c_red8[1], x);
+  r = fma(kd, c_red8[2], r);
+  const double z = r * r;
+  double ps = fma(z, c_s16[3], c_s16[2]);
+  ps = fma(ps, z, c_s16[1]);
+  ps = fma(ps, z, c_s16[0]);
+  const double sr = fma(r * z, ps, r);
+  double pc = fma(z, c_c16[4], c_c16[3]);
+  pc = fma(pc, z, c_c16[2]);
+  pc = fma(pc, z, c_c16[1]);
+  pc = fma(pc, z, c_c16[0]);
+  const double cr = fma(pc, z, 1.0);
+  const double tc = s_cos16[q], ts = s_sin16[q];
+  *c_out = fma(tc, cr, -(ts * sr));
+  *s_out = fma(ts, cr, tc * sr);
+}
+
+__device__ __forceinline__ void dev_sincos(double x, double* c_out, double* s_out) {
+#if UWB_NLI_SINCOS_TABLE
+  dev_sincos_table(x, c_out, s_out);
+#else
+  dev_sincos_quadrant(x, c_out, s_out);
+#endif
+}
+
 // |sum over spans & steps|^2 for one point, computed by one 16-lane segment.
 // Lane sl owns the K consecutive steps m = sl K + b (lane_pos layout, so for
 // each b the segment's 16 loads of a column are one 128-byte line).
@@ -180,10 +233,15 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
                                                const double (&Zr)[K], const double (&Hr)[K]) {
   constexpr int NS = 16 * K;
   const int N = P.steps;
-  const double phi = S.phi[idx];
-  const double w0 = S.w[0][idx], w1 = S.w[1][idx], w2 = S.w[2][idx];
-  const double w3 = S.w[3][idx], w4 = S.w[4][idx], w5 = S.w[5][idx];
-  const int oa = S.col[0][idx] + sl, ob = S.col[1][idx] + sl, oc = S.col[2][idx] + sl;
+  const PointRec& R = S.pt[idx];
+  const double2 wa = *reinterpret_cast<const double2*>(&R.w[0]);
+  const double2 wb = *reinterpret_cast<const double2*>(&R.w[2]);
+  const double2 wc = *reinterpret_cast<const double2*>(&R.w[4]);
+  const double2 ph = *reinterpret_cast<const double2*>(&R.phi);
+  const int4 cl = *reinterpret_cast<const int4*>(&R.col[0]);
+  const double phi = ph.x;
+  const double w0 = wa.x, w1 = wa.y, w2 = wb.x, w3 = wb.y, w4 = wc.x, w5 = wc.y;
+  const int oa = cl.x + sl, ob = cl.y + sl, oc = cl.z + sl;
   double fre = 0.0, fim = 0.0, sre = 0.0, sim = 0.0;
   const int n_spans = HOIST ? 1 : P.n_spans;
   for (int k = 0; k < n_spans; ++k) {
@@ -274,7 +332,7 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
     }
   }
   // fast spans contribute (sum / (j phi)) (gn_integral.hpp:173-175)
-  const double invphi = S.invphi[idx];
+  const double invphi = ph.y;
   double re = fma(fim, invphi, sre);
   double im = fma(-fre, invphi, sim);
 #pragma unroll
@@ -288,7 +346,11 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
 template <int K, bool FULL, bool HOIST>
 __global__ void __launch_bounds__(kWarps * 32, UWB_NLI_MIN_BLOCKS) nli_rows_kernel(const NliParams P) {
   __shared__ WarpSmem s_w[kWarps];
-  if (threadIdx.x < 16) s_exp2_tab[threadIdx.x] = c_exp2_tab16[threadIdx.x];
+  if (threadIdx.x < 16) {
+    s_exp2_tab[threadIdx.x] = c_exp2_tab16[threadIdx.x];
+    s_cos16[threadIdx.x] = c_tab_cos16[threadIdx.x];
+    s_sin16[threadIdx.x] = c_tab_sin16[threadIdx.x];
+  }
   __syncthreads();
 
   constexpr int NS = 16 * K;
@@ -408,16 +470,17 @@ __global__ void __launch_bounds__(kWarps * 32, UWB_NLI_MIN_BLOCKS) nli_rows_kern
         // Column i0 + 1 is always read: clamped stencils have hw1 = 0 and the
         // table carries a zero pad column n.
         const int pos = fast ? __popc(fm & lt) : __popc(fm) + __popc(sm & lt);
-        S.col[0][pos] = st1.i0 * NS;
-        S.col[1][pos] = st2.i0 * NS;
-        S.col[2][pos] = st3.i0 * NS;
-        S.w[0][pos] = st1.hw0 * 16.0; S.w[1][pos] = st1.hw1 * 16.0;
-        S.w[2][pos] = st2.hw0 * 16.0; S.w[3][pos] = st2.hw1 * 16.0;
-        S.w[4][pos] = st3.hw0 * 16.0; S.w[5][pos] = st3.hw1 * 16.0;
-        S.phi[pos] = phi;
-        S.invphi[pos] = phi != 0.0 ? 1.0 / phi : 0.0;
-        S.pw[pos] = pw;
-        S.src[pos] = lane;
+        PointRec& R = S.pt[pos];
+        R.col[0] = st1.i0 * NS;
+        R.col[1] = st2.i0 * NS;
+        R.col[2] = st3.i0 * NS;
+        R.src = lane;
+        R.w[0] = st1.hw0 * 16.0; R.w[1] = st1.hw1 * 16.0;
+        R.w[2] = st2.hw0 * 16.0; R.w[3] = st2.hw1 * 16.0;
+        R.w[4] = st3.hw0 * 16.0; R.w[5] = st3.hw1 * 16.0;
+        R.phi = phi;
+        R.invphi = phi != 0.0 ? 1.0 / phi : 0.0;
+        R.pw = pw;
       }
       __syncwarp();
       const int n_act = __popc(am);
@@ -429,7 +492,7 @@ __global__ void __launch_bounds__(kWarps * 32, UWB_NLI_MIN_BLOCKS) nli_rows_kern
         const bool valid = base + seg < n_act;
         const int idx = valid ? base + seg : base;
         const double kv = point_kernel<K, FULL, HOIST>(P, S, idx, probe, sl, segmask, Zr, Hr);
-        if (valid && sl == 0) S.val[S.src[idx]] = S.pw[idx] * kv;
+        if (valid && sl == 0) S.val[S.pt[idx].src] = S.pt[idx].pw * kv;
       }
       __syncwarp();
       if (lane == 0) {

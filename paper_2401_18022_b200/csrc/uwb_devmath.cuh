@@ -250,4 +250,31 @@ UWB_HD void sincos_rd(double x, double* c_out, double* s_out) {
   *s_out = so;
 }
 
+// 16-entry full-circle sincos (nli_kernel.cu dev_sincos_table): x = k pi/8 + r.
+constexpr double kEightOverPi = 2.5464790894703253723;
+constexpr double kPio8Hi = 0.39269908169872414;      // RN(pi/8)
+constexpr double kPio8Lo = 1.5308084989341915e-17;   // RN(pi/8 - kPio8Hi)
+// sin r = r + r^3 S(r^2), minimax deg 3 on r^2 in [0, (pi/16)^2]
+constexpr double kS16c1 = -0.1666666666666662344925285;
+constexpr double kS16c2 = 0.008333333332974616029035064;
+constexpr double kS16c3 = -0.0001984126518883108036053884;
+constexpr double kS16c4 = 0.000002753800903667705587684024;
+// cos r = 1 + r^2 C(r^2), minimax deg 4
+constexpr double kC16c0 = -0.4999999999999999996528941;
+constexpr double kC16c1 = 0.04166666666666621649926084;
+constexpr double kC16c2 = -0.001388888888795474470406861;
+constexpr double kC16c3 = 0.00002480158051684238140842294;
+constexpr double kC16c4 = -0.0000002753720453432431172966888;
+// cos(k pi/8), sin(k pi/8), k = 0..15, correctly rounded
+#define UWB_COS_TABLE16                                                                     \
+  {1.0, 0.92387953251128674, 0.70710678118654757, 0.38268343236508978, 0.0,                 \
+   -0.38268343236508978, -0.70710678118654757, -0.92387953251128674, -1.0,                  \
+   -0.92387953251128674, -0.70710678118654757, -0.38268343236508978, 0.0,                   \
+   0.38268343236508978, 0.70710678118654757, 0.92387953251128674}
+#define UWB_SIN_TABLE16                                                                     \
+  {0.0, 0.38268343236508978, 0.70710678118654757, 0.92387953251128674, 1.0,                 \
+   0.92387953251128674, 0.70710678118654757, 0.38268343236508978, 0.0,                      \
+   -0.38268343236508978, -0.70710678118654757, -0.92387953251128674, -1.0,                  \
+   -0.92387953251128674, -0.70710678118654757, -0.38268343236508978}
+
 }  // namespace uwb
