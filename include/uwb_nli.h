@@ -197,6 +197,9 @@ int uwb_evaluate_link_resident_noise(uwb_ctx* ctx, const double* psd_dev, void* 
 int uwb_evaluate_link_resident_report(uwb_ctx* ctx, double* report_dev, void* stream);
 int uwb_link_eta_buffer(uwb_ctx* ctx, double** eta_dev, int* n_ch);
 int uwb_resident_status(uwb_ctx* ctx);
+/* Device time (ms) of the last evaluation's Raman ODE stage and its number
+ * of RHS evaluations (prepared/resident path; synchronises). */
+int uwb_last_ode_stats(uwb_ctx* ctx, double* ode_ms, long long* rhs_evals);
 /* Host<->device bytes moved by the last public call. */
 int uwb_last_transfer_bytes(uwb_ctx* ctx, unsigned long long* h2d, unsigned long long* d2h);
 /* Live FP64 FMA-pipe peak of this device, TFLOP/s (roofline denominator). */

@@ -548,6 +548,20 @@ int uwb_link_eta_buffer(uwb_ctx* c, double** eta_dev, int* n_ch) {
   return UWB_OK;
 }
 
+int uwb_last_ode_stats(uwb_ctx* c, double* ode_ms, long long* rhs_evals) {
+  if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
+  uwb_ctx::Prepared* pr = c->prep;
+  float ms = 0.f;
+  if (cudaEventSynchronize(c->evk0) != cudaSuccess ||
+      cudaEventElapsedTime(&ms, c->ev0, c->evk0) != cudaSuccess)
+    ms = 0.f;
+  long long n = 0;
+  xfer_sync(c, &n, pr->d_rhs, sizeof n, cudaMemcpyDeviceToHost);
+  if (ode_ms) *ode_ms = ms;
+  if (rhs_evals) *rhs_evals = n;
+  return UWB_OK;
+}
+
 int uwb_resident_status(uwb_ctx* c) {
   if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
   return check_status(c);

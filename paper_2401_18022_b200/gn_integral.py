@@ -293,6 +293,13 @@ class Engine:
         N.check(self.lib.uwb_fp64_peak(self.h, N.C.byref(t)))
         return t.value
 
+    def last_ode_stats(self):
+        """Raman ODE stage of the last prepared/resident evaluation:
+        {"ode_ms", "rhs_evals"} (synchronises)."""
+        a, b = N.C.c_double(), N.C.c_longlong()
+        N.check(self.lib.uwb_last_ode_stats(self.h, N.C.byref(a), N.C.byref(b)))
+        return {"ode_ms": a.value, "rhs_evals": b.value}
+
     def last_nli_stats(self):
         a, b, c = N.C.c_double(), N.C.c_double(), N.C.c_double()
         N.check(self.lib.uwb_last_nli_stats(self.h, N.C.byref(a), N.C.byref(b), N.C.byref(c)))

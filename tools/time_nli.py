@@ -31,7 +31,7 @@ st = torch.cuda.Stream()
 torch.cuda.set_stream(st)
 psd = torch.tensor(grid.psd, dtype=torch.float64, device="cuda:0")
 rep = torch.zeros(res.report_len, dtype=torch.float64, device="cuda:0")
-ks, ts = [], []
+ks, ts, os_ = [], [], []
 for i in range(a.reps + 2):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
@@ -40,11 +40,15 @@ for i in range(a.reps + 2):
     torch.cuda.synchronize()
     if i >= 2:
         ks.append(eng.last_nli_stats()["kernel_ms"])
+        os_.append(eng.last_ode_stats())
         ts.append(e0.elapsed_time(e1))
 res.check_status()
 n = grid.size()
 eta = rep[:n].cpu().numpy()
 print(json.dumps({"tag": a.tag, "n_r": a.n_r, "density": a.density,
-                  "nli_ms": float(np.median(ks)), "eval_ms": float(np.median(ts)),
+                  "nli_ms": float(np.median(ks)),
+                  "ode_ms": float(np.median([o["ode_ms"] for o in os_])),
+                  "ode_rhs": os_[-1]["rhs_evals"],
+                  "ode_us_per_rhs": float(np.median([o["ode_ms"] for o in os_])) * 1e3 / max(1, os_[-1]["rhs_evals"]), "eval_ms": float(np.median(ts)),
                   "eta_sum": float(np.sum(eta)), "eta_max": float(np.max(eta)),
                   "loss": float(rep[4 * n].item())}), flush=True)
