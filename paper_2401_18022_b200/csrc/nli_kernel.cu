@@ -530,28 +530,43 @@ __global__ void probe_halflog_kernel(const NliParams P) {
 }
 
 // Kahan sum over rows in ascending i per quadrant (gn_integral.hpp:258,306),
-// Q4 mirror (:310) and G = 16/27 gamma^2 sum_q (:312).
+// Q4 mirror (:310) and G = 16/27 gamma^2 sum_q (:312).  One CTA per probe,
+// one warp per quadrant: the warp stages its n_r row sums in shared memory
+// with coalesced loads, then lane 0 runs the (inherently sequential) Kahan
+// sum from shared memory.
 __global__ void finalize_probes_kernel(const NliParams P, const FinalizeParams F) {
-  const int probe = blockIdx.x * blockDim.x + threadIdx.x;
-  if (probe >= F.n_probes) return;
-  double quad[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int q = 0; q < P.n_q; ++q) {
+  extern __shared__ double fin_smem[];
+  const int probe = blockIdx.x;
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ double quad[4];
+  if (q < P.n_q) {
+    double* rs_s = fin_smem + q * P.n_r;
     const double* rs = P.rowsum + (static_cast<size_t>(probe) * P.n_q + q) * P.n_r;
-    double sum = 0.0, comp = 0.0;
-    for (int i = 0; i < P.n_r; ++i) {
-      const double x = rs[i];
-      if (isnan(x)) continue;
-      const double y = x - comp;
-      const double t = sum + y;
-      comp = (t - sum) - y;
-      sum = t;
+    for (int i = lane; i < P.n_r; i += 32) rs_s[i] = rs[i];
+    __syncwarp();
+    if (lane == 0) {
+      double sum = 0.0, comp = 0.0;
+      for (int i = 0; i < P.n_r; ++i) {
+        const double x = rs_s[i];
+        if (isnan(x)) continue;
+        const double y = x - comp;
+        const double t = sum + y;
+        comp = (t - sum) - y;
+        sum = t;
+      }
+      quad[q] = sum;
     }
-    quad[q] = sum;
+  } else if (lane == 0 && q < 4) {
+    quad[q] = 0.0;
   }
-  if (F.mirror_q4) quad[3] = quad[1];
-  const double g = F.probe_gamma[probe];
-  F.probe_g[probe] = (16.0 / 27.0) * g * g * (quad[0] + quad[1] + quad[2] + quad[3]);
-  for (int q = 0; q < 4; ++q) F.probe_quad[4 * probe + q] = quad[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double qd[4] = {quad[0], quad[1], quad[2], P.n_q > 3 ? quad[3] : 0.0};
+    if (F.mirror_q4) qd[3] = qd[1];
+    const double g = F.probe_gamma[probe];
+    F.probe_g[probe] = (16.0 / 27.0) * g * g * (qd[0] + qd[1] + qd[2] + qd[3]);
+    for (int k = 0; k < 4; ++k) F.probe_quad[4 * probe + k] = qd[k];
+  }
 }
 
 // channel_nli + the all_channels_nli epilogue (gn_integral.hpp:316-359).
@@ -681,7 +696,11 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
   k<<<grid_ctas, kWarps * 32, 0, stream>>>(p);
   ++launches;
   if (ev_k1) cudaEventRecord(ev_k1, stream);
-  finalize_probes_kernel<<<(f.n_probes + 127) / 128, 128, 0, stream>>>(p, f);
+  const size_t fin_smem = static_cast<size_t>(p.n_q) * p.n_r * sizeof(double);
+  if (fin_smem > 48 * 1024)
+    cudaFuncSetAttribute(finalize_probes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(fin_smem));
+  finalize_probes_kernel<<<f.n_probes, 128, fin_smem, stream>>>(p, f);
   ++launches;
   if (f.n_ch > 0) {
     finalize_channels_kernel<<<(f.n_ch + 127) / 128, 128, 0, stream>>>(f);

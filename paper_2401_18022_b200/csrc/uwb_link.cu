@@ -98,31 +98,39 @@ __global__ void __launch_bounds__(kTotalsThreads) link_totals_kernel(LinkDev L) 
     sb[i] = L.band ? L.band[i] : -1;
   }
   __syncthreads();
-  if (threadIdx.x != 0) return;
+  // thread 0: loss, capacity, total power; thread 32 + b (another warp, so
+  // the loops run concurrently): band b.  Each sum runs over the channels in
+  // ascending order, like the reference's loop.
   const int nb = L.n_bands < kMaxBands ? L.n_bands : kMaxBands;
-  double bp[kMaxBands], bc[kMaxBands];
-#pragma unroll
-  for (int b = 0; b < kMaxBands; ++b) bp[b] = bc[b] = 0.0;
-  double loss = 0.0, cap = 0.0, total_w = 0.0;
-  for (int i = 0; i < L.n; ++i) {
-    const double p = sp[i];
-    if (p < 0.0) continue;
-    loss -= sl[i];
-    cap += sc[i];
-    total_w += p;
-    const int b = sb[i];
-#pragma unroll
-    for (int k = 0; k < kMaxBands; ++k)
-      if (k == b && k < nb) {
-        bp[k] += p;
-        bc[k] += sc[i];
-      }
-  }
   double* op = L.out + 4 * L.n + 3;
   double* oc = op + L.n_bands;
-  for (int b = 0; b < L.n_bands; ++b) {
-    op[b] = b < nb && bp[b] > 0.0 ? 10.0 * log10(bp[b] / 1e-3) : -300.0;
-    oc[b] = b < nb ? bc[b] : 0.0;
+  if (threadIdx.x >= 32 && threadIdx.x < 32 + nb) {
+    const int b = threadIdx.x - 32;
+    double bp = 0.0, bc = 0.0;
+    // branch-free (adding an exact 0.0 leaves a sum unchanged), so the loads
+    // of successive channels pipeline
+#pragma unroll 8
+    for (int i = 0; i < L.n; ++i) {
+      const bool in = sp[i] >= 0.0 && sb[i] == b;
+      bp += in ? sp[i] : 0.0;
+      bc += in ? sc[i] : 0.0;
+    }
+    op[b] = bp > 0.0 ? 10.0 * log10(bp / 1e-3) : -300.0;
+    oc[b] = bc;
+  }
+  for (int b = nb + threadIdx.x; b < L.n_bands; b += blockDim.x) {  // beyond kMaxBands
+    op[b] = -300.0;
+    oc[b] = 0.0;
+  }
+  if (threadIdx.x != 0) return;
+  double loss = 0.0, cap = 0.0, total_w = 0.0;
+#pragma unroll 8
+  for (int i = 0; i < L.n; ++i) {
+    const double p = sp[i];
+    const bool act = p >= 0.0;
+    loss -= act ? sl[i] : 0.0;
+    cap += act ? sc[i] : 0.0;
+    total_w += act ? p : 0.0;
   }
   L.out[4 * L.n + 0] = loss;
   L.out[4 * L.n + 1] = cap;
