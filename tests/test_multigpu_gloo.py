@@ -82,3 +82,60 @@ def test_two_rank_allreduce_is_bit_identical():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert np.array_equal(got, want)
+
+
+def _gpu_worker(rank, world, port, q):
+    """One rank of the real sharded evaluation: the engine's kernels on cuda:0
+    (both ranks share the one GPU of the test box -- their kernels never wait
+    on each other; the exchange is a host-side gloo all-reduce), then the
+    same all-reduce + SNR report as bench.py's NCCL path."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2401_18022_b200 as uwb
+    from paper_2401_18022_b200.multigpu import ShardedLink
+
+    torch.cuda.set_device(0)
+    eng = uwb.Engine(0)
+    grid = uwb.make_default_uwb_grid()
+    uwb.set_uniform_launch(grid, 1e-3)
+    lc = uwb.LinkConfig(gn=uwb.GnSolverConfig(n_r=24, mean_step_density=0.95))
+    sh = ShardedLink(uwb.default_fibre(), grid, lc, rank, world, engine=eng)
+    st = torch.cuda.Stream()
+    psd = torch.tensor(grid.psd, dtype=torch.float64, device="cuda:0")
+    rep = torch.zeros(sh.report_len, dtype=torch.float64, device="cuda:0")
+    with torch.cuda.stream(st):
+        sh.run(psd.data_ptr(), rep.data_ptr(), st.cuda_stream)
+    torch.cuda.synchronize()
+    sh.check_status()
+    if rank == 0:
+        q.put(rep.cpu().numpy().copy())
+    dist.barrier()
+    dist.destroy_process_group()
+    eng.close()
+
+
+@pytest.mark.gpu
+def test_two_rank_sharded_link_matches_single_gpu():
+    import paper_2401_18022_b200 as uwb
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    eng = uwb.Engine(0)
+    grid = uwb.make_default_uwb_grid()
+    uwb.set_uniform_launch(grid, 1e-3)
+    lc = uwb.LinkConfig(gn=uwb.GnSolverConfig(n_r=24, mean_step_density=0.95))
+    one = uwb.evaluate_link(uwb.default_fibre(), grid, lc, engine=eng)
+    eng.close()
+    n = grid.size()
+    assert np.array_equal(got[:n], one.eta)          # bit-identical eta
+    assert np.array_equal(got[2 * n:3 * n], one.snr_db)
+    assert got[4 * n] == one.loss_value
