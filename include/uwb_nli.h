@@ -140,6 +140,9 @@ typedef struct {
 const char* uwb_last_error(void);
 int uwb_abi_version(void);
 
+/* Visible CUDA devices (the multi-GPU optimiser gives each one a context). */
+int uwb_device_count(int* n);
+
 /* Context: binds one CUDA device (0-based index within CUDA_VISIBLE_DEVICES). */
 int uwb_ctx_create(int device, uwb_ctx** out);
 void uwb_ctx_destroy(uwb_ctx* ctx);
@@ -188,6 +191,15 @@ int uwb_evaluate_link_prepare(uwb_ctx* ctx, const uwb_grid* grid, const uwb_fibr
                               const uwb_link_cfg* link, const uwb_nli_cfg* cfg);
 int uwb_evaluate_link_resident(uwb_ctx* ctx, const double* psd_dev, double* report_dev,
                                void* stream);
+/* n_eval full evaluations of the prepared link back to back on the device
+ * (optimise_launch_powers' value + forward-difference gradient calls,
+ * link_optimizer.hpp:294-309): psd_host [n_eval][n_ch] launch PSDs (W/Hz) in,
+ * loss_host [n_eval] (may be NULL) and report_host [n_eval][report_len] (may
+ * be NULL; layout of uwb_evaluate_link_resident) out.  One upload, one
+ * download, one synchronisation per batch; the first SolverError of the
+ * batch is reported. */
+int uwb_evaluate_link_many(uwb_ctx* ctx, int n_eval, const double* psd_host, double* loss_host,
+                           double* report_host);
 /* Split resident evaluation for multi-GPU runs: the noise stage (Raman ODE +
  * NLI of this context's channel subset) leaves eta in the buffer returned by
  * uwb_link_eta_buffer (zeros outside the subset); the caller all-reduces it

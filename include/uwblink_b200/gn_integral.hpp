@@ -10,6 +10,10 @@
 //   uwblink::b200::solve_power_evolution  <- uwblink::solve_power_evolution  raman_power.hpp:52-55
 //   uwblink::b200::solve_link_noise       <- uwblink::solve_link_noise       link_optimizer.hpp:181-190
 //   uwblink::b200::evaluate_link          <- uwblink::evaluate_link          link_optimizer.hpp:241-245
+//   uwblink::b200::optimise_launch_powers <- uwblink::optimise_launch_powers link_optimizer.hpp:257-324
+//       (the reference's own L-BFGS-B, minimize_bounded lbfgsb.hpp:78, drives
+//        device-resident evaluations; each forward-difference gradient is ONE
+//        batch per GPU, its n_vars evaluations dealt across all visible GPUs)
 //
 // Errors are rethrown as the reference's own uwblink::ConfigError /
 // uwblink::SolverError (units.hpp:16-24), so CLI exit codes 2/3 are kept
@@ -26,8 +30,10 @@
 #include <cstdint>
 #include <memory>
 #include <mutex>
+#include <optional>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "uwb_nli.h"
@@ -338,6 +344,156 @@ inline FibreSamples fibre_samples(const FibreSpec& fibre, const ChannelGrid& gri
   o.rho_end = out.rho_end.data();
   check(uwb_evaluate_link(engine().get(), &g, &fs.f, &lk, &c, &o));
   return out;
+}
+
+namespace detail {
+
+// Everything uwb_evaluate_link_prepare needs for (fibre, grid, plan, cfg, gn).
+struct LinkSetup {
+  FibreSamples fs;
+  std::vector<double> nf;
+  std::vector<int> band;
+  uwb_link_cfg lk{};
+  uwb_nli_cfg c{};
+  LinkSetup(const FibreSpec& fibre, const ChannelGrid& grid, const BandPlan& plan,
+            const LinkConfig& cfg, const GnSolverConfig& gn)
+      : fs(fibre_samples(fibre, grid)), nf(grid.size(), 5.0), band(grid.size(), -1) {
+    for (std::size_t i = 0; i < grid.size(); ++i) {
+      band[i] = plan.band_of_lambda(freq_to_lambda(grid.freq[i]));
+      if (band[i] >= 0) nf[i] = plan.bands[static_cast<std::size_t>(band[i])].nf_db;
+    }
+    lk.include_raman = cfg.raman.include_raman ? 1 : 0;
+    lk.rtol = cfg.raman.rtol;
+    lk.atol = cfg.raman.atol;
+    lk.density = gn.mean_step_density;
+    lk.nf_db = nf.data();
+    lk.band = band.data();
+    lk.n_bands = static_cast<int>(plan.bands.size());
+    lk.use_snr_trx = cfg.use_snr_trx ? 1 : 0;
+    lk.snr_trx_db = cfg.snr_trx_db;
+    c = cfg_view(gn);
+  }
+};
+
+}  // namespace detail
+
+struct OptimiseOptions {
+  int n_devices = 0;               // GPUs for the gradient batches; 0 = all visible
+  long long* cost_evals = nullptr;  // out (optional): full SNR evaluations issued
+};
+
+// optimise_launch_powers (link_optimizer.hpp:257-324) with the reference's
+// own profile helpers and L-BFGS-B; the cost calls run on the device.
+[[nodiscard]] inline OptimiseOutcome optimise_launch_powers(const FibreSpec& fibre,
+                                                            const ChannelGrid& grid0,
+                                                            const BandPlan& plan,
+                                                            const LinkConfig& cfg,
+                                                            double initial_dbm,
+                                                            const OptimiseOptions& opt) {
+  SegmentProfile prof = make_segment_profile(grid0, plan);
+  prof.set_all(initial_dbm);
+  const std::size_t n_vars = cfg.uniform_mode ? 1 : prof.variable_count();
+  std::vector<double> x0(n_vars, initial_dbm);
+  const std::vector<double> lo(n_vars, cfg.bound_lo_dbm);
+  const std::vector<double> hi(n_vars, cfg.bound_hi_dbm);
+  std::vector<GnSolverConfig> phases = cfg.phases;
+  if (phases.empty()) phases.push_back(cfg.gn);
+
+  int n_dev = opt.n_devices;
+  if (n_dev <= 0) check(uwb_device_count(&n_dev));
+  n_dev = std::max(1, n_dev);
+  std::vector<std::unique_ptr<Engine>> eng;
+  eng.reserve(static_cast<std::size_t>(n_dev));
+  for (int d = 0; d < n_dev; ++d) eng.push_back(std::make_unique<Engine>(d));
+
+  OptimiseOutcome out;
+  auto to_profile = [&](const std::vector<double>& v) {
+    if (cfg.uniform_mode) {
+      prof.set_all(v[0]);
+    } else {
+      prof.unflatten(v);
+    }
+  };
+  auto psd_of = [&](const std::vector<double>& v) {
+    to_profile(v);
+    ChannelGrid g = grid0;
+    apply_profile(g, prof, plan);
+    return g;
+  };
+
+  BoundedLbfgsResult best;
+  for (const GnSolverConfig& phase_gn : phases) {
+    ChannelGrid g0 = psd_of(x0);
+    grid0.validate();
+    const detail::LinkSetup setup(fibre, g0, plan, cfg, phase_gn);
+    const uwb_grid gv = detail::grid_view(g0);
+    for (auto& e : eng) check(uwb_evaluate_link_prepare(e->get(), &gv, &setup.fs.f, &setup.lk, &setup.c));
+    std::optional<LinkNoise> frozen;
+    if (cfg.freeze_eta) frozen = b200::solve_link_noise(fibre, g0, cfg, phase_gn);
+    const std::size_t n = grid0.size();
+    // losses of a batch of launch-power vectors, dealt over the GPUs
+    auto losses = [&](const std::vector<std::vector<double>>& vs) {
+      std::vector<double> f(vs.size(), 0.0);
+      if (opt.cost_evals) *opt.cost_evals += static_cast<long long>(vs.size());
+      if (frozen) {
+        for (std::size_t k = 0; k < vs.size(); ++k)
+          f[k] = assemble_link_report(fibre, psd_of(vs[k]), plan, cfg, *frozen).loss_value;
+        return f;
+      }
+      std::vector<double> psd(vs.size() * n);
+      for (std::size_t k = 0; k < vs.size(); ++k) {
+        const ChannelGrid g = psd_of(vs[k]);
+        std::copy(g.psd.begin(), g.psd.end(), psd.begin() + k * n);
+      }
+      const std::size_t per = (vs.size() + eng.size() - 1) / eng.size();
+      std::vector<int> rc(eng.size(), UWB_OK);
+      std::vector<std::string> msg(eng.size());
+      std::vector<std::thread> th;
+      for (std::size_t d = 0; d < eng.size(); ++d) {
+        const std::size_t b = d * per, e = std::min(vs.size(), b + per);
+        if (b >= e) break;
+        th.emplace_back([&, d, b, e] {
+          rc[d] = uwb_evaluate_link_many(eng[d]->get(), static_cast<int>(e - b), psd.data() + b * n,
+                                         f.data() + b, nullptr);
+          if (rc[d]) msg[d] = uwb_last_error();
+        });
+      }
+      for (auto& t : th) t.join();
+      for (std::size_t d = 0; d < eng.size(); ++d) {
+        if (rc[d] == UWB_CONFIG_ERROR) throw ConfigError(msg[d]);
+        if (rc[d] == UWB_SOLVER_ERROR) throw SolverError(msg[d]);
+        if (rc[d]) throw DeviceError(msg[d]);
+      }
+      return f;
+    };
+    auto value = [&](const std::vector<double>& v) { return losses({v})[0]; };
+    auto gradient = [&](const std::vector<double>& v, double f0) {
+      std::vector<std::vector<double>> vs(v.size(), v);
+      for (std::size_t i = 0; i < v.size(); ++i) vs[i][i] += cfg.fd_step_db;
+      const std::vector<double> f = losses(vs);
+      std::vector<double> g(v.size());
+      for (std::size_t i = 0; i < v.size(); ++i) g[i] = (f[i] - f0) / cfg.fd_step_db;
+      return g;
+    };
+    best = minimize_bounded(value, gradient, x0, lo, hi, cfg.lbfgs);
+    out.phase_objectives.push_back(best.f);
+    x0 = best.x;
+  }
+  to_profile(best.x);
+  out.profile = prof;
+  out.solver = best;
+  ChannelGrid g = grid0;
+  apply_profile(g, prof, plan);
+  out.report = b200::evaluate_link(fibre, g, plan, cfg, phases.back());
+  return out;
+}
+
+[[nodiscard]] inline OptimiseOutcome optimise_launch_powers(const FibreSpec& fibre,
+                                                            const ChannelGrid& grid0,
+                                                            const BandPlan& plan,
+                                                            const LinkConfig& cfg,
+                                                            double initial_dbm = 0.0) {
+  return optimise_launch_powers(fibre, grid0, plan, cfg, initial_dbm, OptimiseOptions{});
 }
 
 }  // namespace uwblink::b200

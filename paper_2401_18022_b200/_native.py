@@ -111,6 +111,8 @@ SIGNATURES = {
     "uwb_evaluate_link_prepare": (C.c_int, [C.c_void_p, C.POINTER(Grid), C.POINTER(Fibre),
                                             C.POINTER(LinkCfg), C.POINTER(NliCfg)]),
     "uwb_evaluate_link_resident": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "uwb_device_count": (C.c_int, [IP]),
+    "uwb_evaluate_link_many": (C.c_int, [C.c_void_p, C.c_int, DP, DP, DP]),
     "uwb_evaluate_link_resident_noise": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "uwb_evaluate_link_resident_report": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "uwb_link_eta_buffer": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), IP]),

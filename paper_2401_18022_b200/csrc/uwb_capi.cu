@@ -267,6 +267,17 @@ const char* uwb_last_error(void) { return g_err.c_str(); }
 
 int uwb_abi_version(void) { return UWB_ABI_VERSION; }
 
+int uwb_device_count(int* n) {
+  if (!n) return set_err(UWB_CONFIG_ERROR, "null output");
+  *n = 0;
+  cudaError_t e = cudaGetDeviceCount(n);
+  if (e != cudaSuccess) {
+    *n = 0;
+    return set_err(UWB_CUDA_ERROR, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  }
+  return UWB_OK;
+}
+
 int uwb_ctx_create(int device, uwb_ctx** out) {
   if (!out) return set_err(UWB_CONFIG_ERROR, "null output");
   *out = nullptr;
@@ -311,7 +322,7 @@ void uwb_ctx_destroy(uwb_ctx* c) {
   for (DBuf* b : {&c->freq, &c->psd, &c->gamma, &c->log2rho, &c->zedge, &c->zstart, &c->zmid, &c->width,
                   &c->wlast, &c->probe_nu, &c->probe_gamma, &c->hl2, &c->rowsum, &c->counter,
                   &c->n_eval, &c->probe_g, &c->probe_quad, &c->chan_probe0, &c->eta, &c->nli_psd,
-                  &c->nli_power, &c->quad, &c->skipped, &c->alpha, &c->aeff, &c->raman_x,
+                  &c->nli_power, &c->quad, &c->skipped, &c->batch_psd, &c->batch_report, &c->alpha, &c->aeff, &c->raman_x,
                   &c->raman_y, &c->nf_db, &c->guard, &c->rho_end, &c->ode_work, &c->report,
                   &c->mid, &c->edge})
     b->release();

@@ -60,6 +60,8 @@ struct uwb_ctx {
   uwb::DBuf probe_nu, probe_gamma, hl2, rowsum, counter, n_eval, probe_g, probe_quad, chan_probe0;
   // per-channel results
   uwb::DBuf eta, nli_psd, nli_power, quad, skipped;
+  // uwb_evaluate_link_many: the batch's launch profiles and reports
+  uwb::DBuf batch_psd, batch_report;
   // link evaluation state (raman ODE + assembly)
   uwb::DBuf alpha, aeff, raman_x, raman_y, nf_db, guard, rho_end, ode_work, report, mid, edge;
   std::vector<int> subset;

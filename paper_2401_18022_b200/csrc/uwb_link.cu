@@ -391,12 +391,13 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
 // Noise stage of one evaluation on the prepared state (solve_link_noise,
 // link_optimizer.hpp:181-190): Raman ODE + NLI for the context's channels.
 // psd_dev = launch PSD (device) or null to keep the prepared one.
-int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st) {
+int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_status = true) {
   uwb_ctx::Prepared* pr = c->prep;
   int launches = 0;
   if (psd_dev && psd_dev != pr->d_psd)
     xfer(c, pr->d_psd, psd_dev, pr->n * sizeof(double), cudaMemcpyDeviceToDevice, st);
-  cudaMemsetAsync(pr->d_status, 0, sizeof(int), st);
+  // (a batch keeps the first failure: atomicExch writes are never cleared)
+  if (reset_status) cudaMemsetAsync(pr->d_status, 0, sizeof(int), st);
   cudaEventRecord(c->ev0, st);
   const int lo = launch_raman_ode(pr->O, pr->P.freq, pr->d_psd, pr->P.bch, pr->d_aeff,
                                   pr->aeff_ref, st);
@@ -434,8 +435,8 @@ int run_report(uwb_ctx* c, cudaStream_t st) {
   return UWB_OK;
 }
 
-int run_prepared(uwb_ctx* c, const double* psd_dev, cudaStream_t st) {
-  int rc = run_noise(c, psd_dev, st);
+int run_prepared(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_status = true) {
+  int rc = run_noise(c, psd_dev, st, reset_status);
   if (rc) return rc;
   const int l = c->last_launches;
   rc = run_report(c, st);
@@ -480,6 +481,42 @@ int uwb_evaluate_link_resident(uwb_ctx* c, const double* psd_dev, double* report
     xfer(c, report_dev, c->prep->L.out, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st);
   }
   return UWB_OK;
+}
+
+int uwb_evaluate_link_many(uwb_ctx* c, int n_eval, const double* psd_host, double* loss_host,
+                           double* report_host) {
+  if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
+  if (n_eval < 0 || (n_eval > 0 && !psd_host)) return fail(UWB_CONFIG_ERROR, "bad batch");
+  cudaSetDevice(c->device);
+  reset_xfer(c);
+  uwb_ctx::Prepared* pr = c->prep;
+  const size_t n = pr->n;
+  const size_t rl = 4 * n + 3 + 2 * pr->L.n_bands;
+  if (n_eval == 0) return UWB_OK;
+  double* d_psd = c->batch_psd.get<double>(n_eval * n);
+  double* d_rep = c->batch_report.get<double>(n_eval * rl);
+  if (!d_psd || !d_rep) return fail(UWB_CUDA_ERROR, "device allocation failed");
+  cudaStream_t st = c->stream;
+  xfer(c, d_psd, psd_host, n_eval * n * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(pr->d_status, 0, sizeof(int), st);
+  int launches = 0;
+  for (int e = 0; e < n_eval; ++e) {
+    int rc = run_prepared(c, d_psd + e * n, st, /*reset_status=*/false);
+    if (rc) return rc;
+    launches += c->last_launches;
+    xfer(c, d_rep + e * rl, pr->L.out, rl * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  }
+  if (loss_host) {  // the loss of each report, one strided copy
+    c->d2h_bytes += n_eval * sizeof(double);
+    cudaMemcpy2DAsync(loss_host, sizeof(double), d_rep + 4 * n, rl * sizeof(double),
+                      sizeof(double), n_eval, cudaMemcpyDeviceToHost, st);
+  }
+  if (report_host)
+    xfer(c, report_host, d_rep, n_eval * rl * sizeof(double), cudaMemcpyDeviceToHost, st);
+  c->last_launches = launches;
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "evaluate_link_many");
+  return check_status(c);
 }
 
 int uwb_evaluate_link(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,

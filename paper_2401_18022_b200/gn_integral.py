@@ -526,6 +526,19 @@ class ResidentLink:
                                                         N.C.c_void_p(report_dev_ptr),
                                                         N.C.c_void_p(stream_ptr)))
 
+    def run_many(self, psd: np.ndarray, reports: bool = False):
+        """uwb_evaluate_link_many: n_eval evaluations back to back on the device
+        (the optimiser's value + finite-difference gradient calls) with one
+        upload and one download.  psd [n_eval, n_ch] host launch PSDs (W/Hz) ->
+        loss [n_eval] (and reports [n_eval, report_len] when asked)."""
+        psd = np.ascontiguousarray(psd, dtype=np.float64).reshape(-1, self.n)
+        ne = psd.shape[0]
+        loss = np.zeros(ne)
+        rep = np.zeros((ne, self.report_len)) if reports else None
+        N.check(self.eng.lib.uwb_evaluate_link_many(self.eng.h, ne, N.dptr(psd), N.dptr(loss),
+                                                    N.dptr(rep) if rep is not None else None))
+        return (loss, rep) if reports else loss
+
     # split form for multi-GPU: noise on this rank's channels, all-reduce eta, report
     def run_noise(self, psd_dev_ptr: int, stream_ptr: int = 0):
         N.check(self.eng.lib.uwb_evaluate_link_resident_noise(

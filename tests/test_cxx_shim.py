@@ -30,3 +30,27 @@ def test_cxx_shim_parity():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failure(s)" in r.stdout
+
+
+OPT = os.path.join(ROOT, "oracle", "_ref", "optimise_b200")
+
+
+@pytest.mark.gpu
+def test_cxx_optimise_matches_reference_optimiser():
+    """Config 5 through the C++ drop-in: the reference's own L-BFGS-B driving
+    device evaluations reaches the reference CPU optimiser's iterate and
+    objective (uniform mode, 3 iterations, N_R=24 so the CPU side is quick)."""
+    import json
+
+    if not os.path.exists(OPT):
+        pytest.skip("oracle/_ref/optimise_b200 not built (needs /root/reference at build time)")
+    r = subprocess.run([OPT, "--iters", "3", "--n-r", "24", "--density", "0.95", "--uniform", "1",
+                        "--reference-iters", "3", "--devices", "1"],
+                       capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout + r.stderr
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    print(d)
+    ref = d["reference"]
+    assert d["lbfgs_iterations"] == ref["lbfgs_iterations"]
+    assert ref["rel_dobjective"] < 1e-9
+    assert ref["max_abs_dx_db"] < 1e-6

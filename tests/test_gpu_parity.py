@@ -215,3 +215,23 @@ def test_resident_link_equals_host_call(golden, engine):
     assert np.array_equal(o[:n], host.eta)
     assert np.array_equal(o[2 * n:3 * n], host.snr_db)
     assert o[4 * n] == host.loss_value
+
+
+def test_evaluate_link_many_equals_single_evaluations(golden, engine):
+    """uwb_evaluate_link_many (the optimiser's batched cost calls) reproduces
+    one-at-a-time evaluations bit for bit, in order."""
+    rec = golden["evaluate_link"]["uwb589_random_launch"]
+    case = Case.from_json(rec["case"])
+    grid, fibre = product_scenario(case)
+    lc = uwb.LinkConfig(gn=uwb.GnSolverConfig(n_r=24, mean_step_density=0.95))
+    res = uwb.ResidentLink(fibre, grid, lc, engine=engine)
+    rng = np.random.default_rng(7)
+    base = np.array(grid.psd)
+    psd = np.stack([base * (1.0 + 0.2 * rng.random(base.size)) * (base > 0) for _ in range(4)])
+    loss, reps = res.run_many(psd, reports=True)
+    for k in range(4):
+        g = grid.copy()
+        g.psd = psd[k].copy()
+        one = uwb.evaluate_link(fibre, g, lc, engine=engine)
+        assert loss[k] == one.loss_value
+        assert np.array_equal(reps[k][:grid.size()], one.eta)
