@@ -306,28 +306,30 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
     } else {
       const double* zm = P.zmid + static_cast<size_t>(k) * NS + sl;
       const double* wd = P.width + static_cast<size_t>(k) * NS + sl;
-#pragma unroll 1
+      // fully unrolled like the fast loop (independent steps interleave);
+      // lanes past N contribute a zero weight
+#pragma unroll
       for (int b = 0; b < K; ++b) {
-        if (FULL || sl * K + b < N) {
-          const int o = 16 * b;
-          double lg = fma(w0, __ldg(ca + o), -__ldg(hl + o));
-          lg = fma(w1, __ldg(ca + NS + o), lg);
-          lg = fma(w2, __ldg(cb + o), lg);
-          lg = fma(w3, __ldg(cb + NS + o), lg);
-          lg = fma(w4, __ldg(cc3 + o), lg);
-          lg = fma(w5, __ldg(cc3 + NS + o), lg);
-          const double p = dev_exp2_16(lg);
-          const double wm = __ldg(wd + o);
-          // sinc(x), |x| = |phi| w / 2 <= 5e-5 here: 1 - x^2/6 + x^4/120 is exact
-          const double x = 0.5 * phi * wm;
-          const double x2 = x * x;
-          const double sinc = fma(x2, fma(x2, 1.0 / 120.0, -1.0 / 6.0), 1.0);
-          const double w = p * wm * sinc;
-          double cs, sn;
-          dev_sincos(phi * __ldg(zm + o), &cs, &sn);
-          sre = fma(w, cs, sre);
-          sim = fma(w, sn, sim);
-        }
+        const int o = 16 * b;
+        const double H = HOIST ? Hr[b] : __ldg(hl + o);
+        double lg = fma(w0, __ldg(ca + o), -H);
+        lg = fma(w1, __ldg(ca + NS + o), lg);
+        lg = fma(w2, __ldg(cb + o), lg);
+        lg = fma(w3, __ldg(cb + NS + o), lg);
+        lg = fma(w4, __ldg(cc3 + o), lg);
+        lg = fma(w5, __ldg(cc3 + NS + o), lg);
+        const double p = dev_exp2_16(lg);
+        const double wm = __ldg(wd + o);
+        // sinc(x), |x| = |phi| w / 2 <= 5e-5 here: 1 - x^2/6 + x^4/120 is exact
+        const double x = 0.5 * phi * wm;
+        const double x2 = x * x;
+        const double sinc = fma(x2, fma(x2, 1.0 / 120.0, -1.0 / 6.0), 1.0);
+        double w = p * wm * sinc;
+        if (!FULL) w = (sl * K + b < N) ? w : 0.0;
+        double cs, sn;
+        dev_sincos(phi * __ldg(zm + o), &cs, &sn);
+        sre = fma(w, cs, sre);
+        sim = fma(w, sn, sim);
       }
     }
   }

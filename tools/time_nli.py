@@ -20,10 +20,16 @@ p.add_argument("--n-r", type=int, default=150)
 p.add_argument("--density", type=float, default=1.4)
 p.add_argument("--reps", type=int, default=7)
 p.add_argument("--tag", default=os.environ.get("UWB_LIB_PATH", "main"))
+p.add_argument("--grid", default="uwb589", choices=["uwb589", "oband11", "cband11"])
 a = p.parse_args()
 eng = uwb.Engine(0)
-grid = uwb.make_default_uwb_grid()
-uwb.set_uniform_launch(grid, 1e-3)
+if a.grid == "uwb589":
+    grid = uwb.make_default_uwb_grid()
+    uwb.set_uniform_launch(grid, 1e-3)
+else:  # BASELINE configs 1/2: 11 x 96 GBd, 100 GHz, at 1550 nm (0 dBm) / 1302.3 nm (2 dBm)
+    lam, dbm = (1550e-9, 0.0) if a.grid == "cband11" else (1302.3e-9, 2.0)
+    grid = uwb.make_uniform_grid(11, 100e9, 96e9, 299792458.0 / lam)
+    uwb.set_uniform_launch(grid, 1e-3 * 10 ** (dbm / 10))
 res = uwb.ResidentLink(uwb.default_fibre(), grid,
                        uwb.LinkConfig(gn=uwb.GnSolverConfig(n_r=a.n_r, mean_step_density=a.density)),
                        engine=eng)
@@ -45,7 +51,7 @@ for i in range(a.reps + 2):
 res.check_status()
 n = grid.size()
 eta = rep[:n].cpu().numpy()
-print(json.dumps({"tag": a.tag, "n_r": a.n_r, "density": a.density,
+print(json.dumps({"tag": a.tag, "grid": a.grid, "n_r": a.n_r, "density": a.density,
                   "nli_ms": float(np.median(ks)),
                   "ode_ms": float(np.median([o["ode_ms"] for o in os_])),
                   "ode_rhs": os_[-1]["rhs_evals"],
