@@ -229,7 +229,7 @@ def run_engine(args):
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    kern_ms = []
+    kern_ms, ode_ms = [], []
     launches = 0
     barrier()
     with ClockSampler(local) as clk:
@@ -241,21 +241,24 @@ def run_engine(args):
             torch.cuda.synchronize(dev)
             launches += n_launch[0]
             kern_ms.append(eng.last_nli_stats()["kernel_ms"])
+            ode_ms.append(eng.last_ode_stats()["ode_ms"])
         barrier()
     res.check_status()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = float(np.sum(step_ms))
     stats = eng.last_nli_stats()
-    t = torch.tensor([total_ms, float(np.mean(kern_ms)), stats["inner_steps"]], dtype=torch.float64,
-                     device=dev)
+    t = torch.tensor([total_ms, float(np.mean(kern_ms)), float(np.mean(ode_ms)), stats["inner_steps"],
+                      stats["active_points"] * stats["inner_steps"] / max(stats["evaluated_points"], 1.0)],
+                     dtype=torch.float64, device=dev)
     if world > 1:
         tmax = t.clone()
-        dist.all_reduce(tmax[:2], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tmax[:3], op=dist.ReduceOp.MAX)
         tsum = t.clone()
-        dist.all_reduce(tsum[2:], op=dist.ReduceOp.SUM)
-        total_ms, kmax, inner = float(tmax[0]), float(tmax[1]), float(tsum[2])
+        dist.all_reduce(tsum[3:], op=dist.ReduceOp.SUM)
+        total_ms, kmax, omax = float(tmax[0]), float(tmax[1]), float(tmax[2])
+        inner, inner_ref = float(tsum[3]), float(tsum[4])
     else:
-        kmax, inner = float(t[1]), float(t[2])
+        kmax, omax, inner, inner_ref = float(t[1]), float(t[2]), float(t[3]), float(t[4])
     ms_per = total_ms / args.steps
     rep = report.cpu().numpy()
     n = grid.size()
@@ -335,6 +338,9 @@ def run_engine(args):
         # per-GPU achieved rate of the integrand kernel (all ranks' steps over
         # the slowest rank's kernel time, divided by the GPU count)
         achieved = FLOPS_PER_STEP * inner / (kmax * 1e-3) / 1e12 / world if kmax > 0 else None
+        # the reference enumerates every active point; symmetric rows (quadrants
+        # 1 and 3) share |K|^2 between u2 and -u2, so fewer steps are computed
+        effective = FLOPS_PER_STEP * inner_ref / (kmax * 1e-3) / 1e12 / world if kmax > 0 else None
         tr = read_traffic()
         line = {
             "metric": METRIC, "value": ms_per / 1e3, "unit": UNIT, "n_gpus": world,
@@ -351,6 +357,9 @@ def run_engine(args):
                          "traffic": tr.get("dram_bytes_per_launch") if tr else None,
                          "kernel": "nli_rows_kernel (GN integrand)",
                          "kernel_ms": kmax, "inner_steps": inner,
+                         "inner_steps_reference": inner_ref,
+                         "effective_tflops_reference_steps": effective,
+                         "ode_ms": omax,
                          "flops_per_step": FLOPS_PER_STEP,
                          "peak_source": "live DFMA microbenchmark (uwb_fp64_peak), this GPU",
                          "kernel_share_of_step": kmax / ms_per if ms_per else None},

@@ -209,6 +209,11 @@ int uwb_evaluate_link_resident_noise(uwb_ctx* ctx, const double* psd_dev, void* 
 int uwb_evaluate_link_resident_report(uwb_ctx* ctx, double* report_dev, void* stream);
 int uwb_link_eta_buffer(uwb_ctx* ctx, double** eta_dev, int* n_ch);
 int uwb_resident_status(uwb_ctx* ctx);
+/* Active points of the last NLI (every point of the reference's enumeration
+ * with three non-zero PSDs); evaluated_points of uwb_last_nli_stats counts
+ * the |K|^2 evaluations actually run (symmetric rows share mirrored ones).
+ * Call after uwb_last_nli_stats. */
+int uwb_last_nli_active(uwb_ctx* ctx, double* active_points);
 /* Device time (ms) of the last evaluation's Raman ODE stage and its number
  * of RHS evaluations (prepared/resident path; synchronises). */
 int uwb_last_ode_stats(uwb_ctx* ctx, double* ode_ms, long long* rhs_evals);

@@ -122,6 +122,7 @@ SIGNATURES = {
     "uwb_fp64_peak": (C.c_int, [C.c_void_p, DP]),
     "uwb_last_launch_count": (C.c_int, [C.c_void_p]),
     "uwb_last_nli_stats": (C.c_int, [C.c_void_p, DP, DP, DP]),
+    "uwb_last_nli_active": (C.c_int, [C.c_void_p, DP]),
     "uwb_last_ode_stats": (C.c_int, [C.c_void_p, DP, C.POINTER(C.c_longlong)]),
     "uwb_model_fibre": (C.c_int, [C.c_int, C.c_double, C.c_int, DP, C.c_double,
                                   C.POINTER(FibreSample)]),

@@ -107,8 +107,9 @@ struct alignas(16) PointRec {
 
 struct WarpSmem {
   PointRec pt[32];
-  double val[32];    // pw * |kernel|^2 per chunk column
-  double nu, f, s1, s2, su, u1, lo, du2, row_acc;
+  double kv[32];     // |kernel|^2 of each chunk lane's evaluated point
+  double nu, f, s1, s2, su, u1, lo, du2;
+  int sym;           // row symmetric under u2 -> -u2 (b1 == b2: quadrants 1, 3)
 };
 
 // Polynomial coefficients as __constant__ data: ptxas keeps them in uniform
@@ -348,6 +349,7 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
 template <int K, bool FULL, bool HOIST>
 __global__ void __launch_bounds__(kWarps * 32, UWB_NLI_MIN_BLOCKS) nli_rows_kernel(const NliParams P) {
   __shared__ WarpSmem s_w[kWarps];
+  extern __shared__ double row_vals[];  // [kWarps][n_r]
   if (threadIdx.x < 16) {
     s_exp2_tab[threadIdx.x] = c_exp2_tab16[threadIdx.x];
     s_cos16[threadIdx.x] = c_tab_cos16[threadIdx.x];
@@ -431,20 +433,36 @@ __global__ void __launch_bounds__(kWarps * 32, UWB_NLI_MIN_BLOCKS) nli_rows_kern
         S.u1 = u1;
         S.lo = lo;
         S.du2 = (hi - lo) / n_r;
-        S.row_acc = 0.0;
+        // quadrants 1 and 3 (s1 == s2, b1 == b2); quadrant 2 at f = 0 has
+        // b1 == b2 too but maps (f1, f2) -> (-f2, -f1): not a symmetry
+        S.sym = (P.mirror_u2 && s1 == s2 && b1 == b2) ? 1 : 0;
       }
       __syncwarp();
     }
-    unsigned n_eval = 0;
-
-    for (int jb = 0; jb < n_r; jb += 32) {
+    unsigned n_eval = 0, n_act_row = 0;
+    double* val_row = row_vals + static_cast<size_t>(warp) * n_r;  // pw |K|^2 per column j
+    // Symmetric rows (quadrants 1 and 3: s1 == s2, b1 == b2): u2 -> -u2 swaps f1 and f2,
+    // and the integrand is symmetric in them (phase_mismatch is bit-exactly
+    // symmetric, gn_integral.hpp:43-50; the power factor is a product over
+    // the three stencils), so column n_r-1-j carries the |K|^2 of column j up
+    // to the few-ulp difference of the recomputed coordinates.  Each column
+    // still gets its own setup (PSD window tests, p1 p2 p3), so the active set
+    // is exactly the reference's; only |K|^2 is shared.  Lanes 0..15 take
+    // columns j, lanes 16..31 their mirrors.
+    const bool sym = S.sym != 0;
+    const int half = sym ? (n_r + 1) / 2 : n_r;
+    const int span = sym ? 16 : 32;
+    for (int jb = 0; jb < half; jb += span) {
       // ---- per-point setup, one u2 column per lane (gn_integral.hpp:288-303)
-      const int j = jb + lane;
+      const int m = sym ? jb + (lane & 15) : jb + lane;
+      const bool primary = !sym || lane < 16;
+      const int j = primary ? m : n_r - 1 - m;
+      const bool valid = m < half && (primary || j != m);
       bool active = false;
       bool fast = false;
       Stencil st1, st2, st3;
       double phi = 0.0, pw = 0.0;
-      if (j < n_r) {
+      if (valid) {
         const double nu = S.nu, su = S.su, u1 = S.u1;
         const double u2 = S.lo + (static_cast<double>(j) + 0.5) * S.du2;
         const double g1 = su * exp(u2);
@@ -463,11 +481,14 @@ __global__ void __launch_bounds__(kWarps * 32, UWB_NLI_MIN_BLOCKS) nli_rows_kern
         }
       }
       const unsigned am = __ballot_sync(kFull, active);
-      const unsigned fm = __ballot_sync(kFull, active && fast);
-      const unsigned sm = am & ~fm;
+      // a mirror column evaluates its own |K|^2 only if its partner is inactive
+      const bool partner_active = sym && ((am >> (lane ^ 16)) & 1u);
+      const bool need = active && (primary || !partner_active);
+      const unsigned nm = __ballot_sync(kFull, need);
+      const unsigned fm = __ballot_sync(kFull, need && fast);
+      const unsigned sm = nm & ~fm;
       const unsigned lt = (1u << lane) - 1u;
-      S.val[lane] = 0.0;
-      if (active) {
+      if (need) {
         // fast points first, then slow ones, so half-warp pairs rarely diverge.
         // Column i0 + 1 is always read: clamped stencils have hw1 = 0 and the
         // table carries a zero pad column n.
@@ -485,30 +506,30 @@ __global__ void __launch_bounds__(kWarps * 32, UWB_NLI_MIN_BLOCKS) nli_rows_kern
         R.pw = pw;
       }
       __syncwarp();
-      const int n_act = __popc(am);
-      n_eval += n_act;
-      int base = 0;
+      const int n_need = __popc(nm);
+      n_eval += n_need;
+      n_act_row += __popc(am);
       // warp-uniform trip count: with an odd count the idle half-warp repeats
       // its partner's point (same branch, result dropped) instead of diverging
-      for (; base < n_act; base += 2) {
-        const bool valid = base + seg < n_act;
-        const int idx = valid ? base + seg : base;
+      for (int base = 0; base < n_need; base += 2) {
+        const bool ok = base + seg < n_need;
+        const int idx = ok ? base + seg : base;
         const double kv = point_kernel<K, FULL, HOIST>(P, S, idx, probe, sl, segmask, Zr, Hr);
-        if (valid && sl == 0) S.val[S.pt[idx].src] = S.pt[idx].pw * kv;
+        if (ok && sl == 0) S.kv[S.pt[idx].src] = kv;
       }
       __syncwarp();
-      if (lane == 0) {
-        const int lim = min(32, n_r - jb);
-        double acc = S.row_acc;
-        for (int t = 0; t < lim; ++t) acc += S.val[t];  // ascending j
-        S.row_acc = acc;
-      }
+      if (valid) val_row[j] = active ? pw * (need ? S.kv[lane] : S.kv[lane ^ 16]) : 0.0;
       __syncwarp();
     }
     if (lane == 0) {
-      P.rowsum[row] = S.row_acc * du1 * S.du2;
+      double acc = 0.0;
+      for (int t = 0; t < n_r; ++t) acc += val_row[t];  // ascending j (gn_integral.hpp:288-305)
+      P.rowsum[row] = acc * du1 * S.du2;
       atomicAdd(P.n_eval, static_cast<unsigned long long>(n_eval));
+      atomicAdd(P.n_active, static_cast<unsigned long long>(n_act_row));
     }
+    __syncwarp();
+
   }
 }
 
@@ -672,11 +693,22 @@ int launch_finalize_channels_only(const FinalizeParams& f, cudaStream_t st) {
   return 1;
 }
 
-int nli_ctas_per_sm(int steps, bool one_span) {
+namespace {
+size_t row_smem(int n_r) { return static_cast<size_t>(kWarps) * n_r * sizeof(double); }
+void allow_row_smem(RowKernel k, int n_r) {
+  if (row_smem(n_r) > 32 * 1024)
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(row_smem(n_r)));
+}
+}  // namespace
+
+int nli_ctas_per_sm(int steps, bool one_span, int n_r) {
   RowKernel k = row_kernel_for(steps, one_span);
   if (!k) return 0;
+  allow_row_smem(k, n_r);
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kWarps * 32, 0) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kWarps * 32, row_smem(n_r)) != cudaSuccess)
+    return 0;
   return n;
 }
 
@@ -691,11 +723,12 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
   if (!k || p.n_probes <= 0 || p.col_stride != 16 * ((p.steps + 15) / 16)) return -1;
   int launches = 0;
   cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), stream);
-  cudaMemsetAsync(p.n_eval, 0, sizeof(unsigned long long), stream);
+  cudaMemsetAsync(p.n_eval, 0, 2 * sizeof(unsigned long long), stream);  // n_eval, n_active
   probe_halflog_kernel<<<p.n_probes, 128, 0, stream>>>(p);
   ++launches;
   if (ev_k0) cudaEventRecord(ev_k0, stream);
-  k<<<grid_ctas, kWarps * 32, 0, stream>>>(p);
+  allow_row_smem(k, p.n_r);
+  k<<<grid_ctas, kWarps * 32, row_smem(p.n_r), stream>>>(p);
   ++launches;
   if (ev_k1) cudaEventRecord(ev_k1, stream);
   const size_t fin_smem = static_cast<size_t>(p.n_q) * p.n_r * sizeof(double);

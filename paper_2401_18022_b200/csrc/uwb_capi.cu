@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -145,6 +146,12 @@ int set_cfg(const uwb_nli_cfg* cfg, NliParams* P) {
   P->u1_uniform = cfg->u1_uniform ? 1 : 0;
   P->ln_min = std::log(cfg->u1_min_ratio);
   P->n_q = cfg->mirror_q4 ? 3 : 4;
+  // UWB_NLI_NO_MIRROR=1 evaluates every column of symmetric rows (A/B checks)
+  static const bool no_mirror = [] {
+    const char* e = std::getenv("UWB_NLI_NO_MIRROR");
+    return e && e[0] == '1';
+  }();
+  P->mirror_u2 = no_mirror ? 0 : 1;
   return UWB_OK;
 }
 
@@ -176,7 +183,8 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
   P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * P.col_stride);
   P.rowsum = c->rowsum.get<double>(std::max(P.total_rows, 1));
   P.counter = c->counter.get<unsigned int>(1);
-  P.n_eval = c->n_eval.get<unsigned long long>(1);
+  P.n_eval = c->n_eval.get<unsigned long long>(2);
+  P.n_active = P.n_eval + 1;
   F.probe_gamma = d_g;
   F.probe_g = c->probe_g.get<double>(std::max(np, 1));
   F.probe_quad = c->probe_quad.get<double>(4 * std::max(np, 1));
@@ -204,7 +212,7 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
   }
   cudaEventRecord(c->ev0, st);
   if (np) {
-    const int per_sm = nli_ctas_per_sm(P.steps, P.n_spans == 1);
+    const int per_sm = nli_ctas_per_sm(P.steps, P.n_spans == 1, P.n_r);
     if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
     const int launched = launch_nli(P, F, c->sm_count * per_sm, st, c->evk0, c->evk1);
     if (launched < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
@@ -224,10 +232,11 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
     if (np) {
       cudaEventElapsedTime(&ms, c->evk0, c->evk1);
       c->last_kernel_ms = ms;
-      unsigned long long ne = 0;
-      xfer_sync(c, &ne, P.n_eval, sizeof ne, cudaMemcpyDeviceToHost);
-      c->last_points = static_cast<double>(ne);
-      c->last_inner_steps = static_cast<double>(ne) * P.steps * P.n_spans;
+      unsigned long long ne[2] = {0, 0};
+      xfer_sync(c, ne, P.n_eval, sizeof ne, cudaMemcpyDeviceToHost);
+      c->last_points = static_cast<double>(ne[0]);
+      c->last_active = static_cast<double>(ne[1]);
+      c->last_inner_steps = static_cast<double>(ne[0]) * P.steps * P.n_spans;
     }
   }
   return UWB_OK;
@@ -306,7 +315,7 @@ int uwb_ctx_create(int device, uwb_ctx** out) {
   cudaEventCreate(&c->evk0);
   cudaEventCreate(&c->evk1);
   // probe the kernel image: fails loudly if the fatbin has no sm_100a code
-  if (nli_ctas_per_sm(112, true) <= 0) {
+  if (nli_ctas_per_sm(112, true, 150) <= 0) {
     uwb_ctx_destroy(c);
     return set_err(UWB_CUDA_ERROR, "integrand kernel not loadable on this device");
   }
@@ -456,14 +465,21 @@ int uwb_last_nli_stats(uwb_ctx* c, double* kernel_ms, double* inner_steps,
         cudaEventElapsedTime(&ms, c->evk0, c->evk1) == cudaSuccess)
       c->last_kernel_ms = ms;
     const unsigned long long* d_ne = c->n_eval.ptr<unsigned long long>();
-    unsigned long long ne = 0;
-    if (d_ne) cudaMemcpy(&ne, d_ne, sizeof ne, cudaMemcpyDeviceToHost);
-    c->last_points = static_cast<double>(ne);
-    c->last_inner_steps = static_cast<double>(ne) * c->last_steps * c->last_spans;
+    unsigned long long ne[2] = {0, 0};
+    if (d_ne) cudaMemcpy(ne, d_ne, sizeof ne, cudaMemcpyDeviceToHost);
+    c->last_points = static_cast<double>(ne[0]);
+    c->last_active = static_cast<double>(ne[1]);
+    c->last_inner_steps = static_cast<double>(ne[0]) * c->last_steps * c->last_spans;
   }
   if (kernel_ms) *kernel_ms = c->last_kernel_ms;
   if (inner_steps) *inner_steps = c->last_inner_steps;
   if (evaluated_points) *evaluated_points = c->last_points;
+  return UWB_OK;
+}
+
+int uwb_last_nli_active(uwb_ctx* c, double* active_points) {
+  if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  if (active_points) *active_points = c->last_active;  // resolved by uwb_last_nli_stats
   return UWB_OK;
 }
 

@@ -73,6 +73,7 @@ struct uwb_ctx {
   double last_kernel_ms = 0.0;
   double last_inner_steps = 0.0;
   double last_points = 0.0;
+  double last_active = 0.0;  // active (reference-enumerated) points of the last NLI
   // pinned host staging for small transfers
   void* pinned = nullptr;
   size_t pinned_cap = 0;

@@ -310,7 +310,8 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * NS);
   P.rowsum = c->rowsum.get<double>(std::max(P.total_rows, 1));
   P.counter = c->counter.get<unsigned int>(1);
-  P.n_eval = c->n_eval.get<unsigned long long>(1);
+  P.n_eval = c->n_eval.get<unsigned long long>(2);
+  P.n_active = P.n_eval + 1;
   FinalizeParams& F = pr->F;
   F.n_probes = np;
   F.probe_gamma = up(c, c->probe_gamma, gam.data(), gam.size());
@@ -380,7 +381,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   L.out = c->report.get<double>(4 * static_cast<size_t>(n) + 3 + 2 * L.n_bands);
   L.tmp = d_tmp;
 
-  const int per_sm = nli_ctas_per_sm(steps, P.n_spans == 1);
+  const int per_sm = nli_ctas_per_sm(steps, P.n_spans == 1, P.n_r);
   if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
   pr->grid_ctas = c->sm_count * per_sm;
   cudaError_t e = cudaStreamSynchronize(c->stream);
@@ -559,10 +560,11 @@ int uwb_evaluate_link(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
     float kms = 0.f;
     cudaEventElapsedTime(&kms, c->evk0, c->evk1);
     c->last_kernel_ms = kms;
-    unsigned long long ne = 0;
-    xfer_sync(c, &ne, pr->P.n_eval, sizeof ne, cudaMemcpyDeviceToHost);
-    c->last_points = static_cast<double>(ne);
-    c->last_inner_steps = static_cast<double>(ne) * pr->P.steps * pr->P.n_spans;
+    unsigned long long ne[2] = {0, 0};
+    xfer_sync(c, ne, pr->P.n_eval, sizeof ne, cudaMemcpyDeviceToHost);
+    c->last_points = static_cast<double>(ne[0]);
+    c->last_active = static_cast<double>(ne[1]);
+    c->last_inner_steps = static_cast<double>(ne[0]) * pr->P.steps * pr->P.n_spans;
   }
   return UWB_OK;
 }

@@ -303,7 +303,10 @@ class Engine:
     def last_nli_stats(self):
         a, b, c = N.C.c_double(), N.C.c_double(), N.C.c_double()
         N.check(self.lib.uwb_last_nli_stats(self.h, N.C.byref(a), N.C.byref(b), N.C.byref(c)))
-        return dict(kernel_ms=a.value, inner_steps=b.value, evaluated_points=c.value)
+        d = N.C.c_double()
+        N.check(self.lib.uwb_last_nli_active(self.h, N.C.byref(d)))
+        return dict(kernel_ms=a.value, inner_steps=b.value, evaluated_points=c.value,
+                    active_points=d.value)
 
 
 _engine: Engine | None = None

@@ -45,7 +45,8 @@ for i in range(a.reps + 2):
     e1.record(st)
     torch.cuda.synchronize()
     if i >= 2:
-        ks.append(eng.last_nli_stats()["kernel_ms"])
+        st_ = eng.last_nli_stats()
+        ks.append(st_["kernel_ms"])
         os_.append(eng.last_ode_stats())
         ts.append(e0.elapsed_time(e1))
 res.check_status()
@@ -53,6 +54,7 @@ n = grid.size()
 eta = rep[:n].cpu().numpy()
 print(json.dumps({"tag": a.tag, "grid": a.grid, "n_r": a.n_r, "density": a.density,
                   "nli_ms": float(np.median(ks)),
+                  "evaluated": st_["evaluated_points"], "active": st_["active_points"],
                   "ode_ms": float(np.median([o["ode_ms"] for o in os_])),
                   "ode_rhs": os_[-1]["rhs_evals"],
                   "ode_us_per_rhs": float(np.median([o["ode_ms"] for o in os_])) * 1e3 / max(1, os_[-1]["rhs_evals"]), "eval_ms": float(np.median(ts)),
