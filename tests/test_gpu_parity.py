@@ -6,12 +6,16 @@ Tolerances (BASELINE.json north_star: <= 1e-6 relative eta, <= 0.01 dB SNR):
   NLI on identical inputs ............ 1e-9 relative (FP64; observed ~1e-13)
   full path (device ODE + NLI + SNR) . 1e-6 relative eta, 0.01 dB SNR
 """
+import os
+
 import numpy as np
 import pytest
 
 import paper_2401_18022_b200 as uwb
 from helpers import cfg_of, engine_inputs_from_oracle, product_scenario, to_db
 from pyoracle import Case, toy_case
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 
@@ -235,3 +239,43 @@ def test_evaluate_link_many_equals_single_evaluations(golden, engine):
         one = uwb.evaluate_link(fibre, g, lc, engine=engine)
         assert loss[k] == one.loss_value
         assert np.array_equal(reps[k][:grid.size()], one.eta)
+
+
+def test_u2_symmetry_sharing_matches_full_evaluation():
+    """Quadrants 1 and 3 share |K|^2 between u2 and -u2; the
+    quadrant sums with sharing off (UWB_NLI_NO_MIRROR=1, every column
+    evaluated) must agree to rounding, on a case with a centre probe (Q2 at
+    f = 0 is NOT a symmetry) and Simpson probes."""
+    import json
+    import subprocess
+    import sys
+
+    code = r'''
+import json, sys
+sys.path.insert(0, "oracle"); sys.path.insert(0, "tests")
+import numpy as np
+import paper_2401_18022_b200 as uwb
+from pyoracle import Oracle, oband11
+from helpers import engine_inputs_from_oracle, cfg_of
+case = oband11(n_r=60, density=0.95)
+case.simpson = 1
+O = Oracle(); prep = O.prepare(case)
+grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
+eng = uwb.Engine(0)
+r = uwb.all_channels_nli(grid, spans, betas, None, cfg_of(case), engine=eng, gamma=gamma)
+st = eng.last_nli_stats()
+print(json.dumps({"q": np.asarray(r.quadrant).ravel().tolist(), "eta": np.asarray(r.eta).tolist(),
+                  "evaluated": st["evaluated_points"], "active": st["active_points"]}))
+'''
+    out = {}
+    for flag in ("0", "1"):
+        env = dict(os.environ, UWB_NLI_NO_MIRROR=flag)
+        p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           timeout=600, cwd=ROOT)
+        assert p.returncode == 0, p.stderr
+        out[flag] = json.loads(p.stdout.strip().splitlines()[-1])
+    on, off = out["0"], out["1"]
+    assert on["active"] == off["active"] == off["evaluated"]
+    assert on["evaluated"] < 0.75 * off["evaluated"]
+    assert _rel(on["q"], off["q"]) < 1e-13
+    assert _rel(on["eta"], off["eta"]) < 1e-13
