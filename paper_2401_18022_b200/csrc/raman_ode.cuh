@@ -44,7 +44,10 @@ int raman_segments(const double* x, const double* y, int rn, double spacing, int
 
 // Fills the per-channel coupling factors from the launch PSD and runs the
 // one-CTA ODE kernel.  Returns kernel launches issued, or < 0 on failure.
+// max_ept > 0 overrides the channels-per-thread choice (5 keeps the 589-ch
+// solve on 128 threads x <= 255 registers: it then fits on an SM beside one
+// integrand CTA, for overlapped batches).
 int launch_raman_ode(OdeParams P, const double* freq, const double* psd, double bch,
-                     const double* aeff, double aeff_ref, cudaStream_t st);
+                     const double* aeff, double aeff_ref, cudaStream_t st, int max_ept = 0);
 
 }  // namespace uwb

@@ -331,11 +331,19 @@ void uwb_ctx_destroy(uwb_ctx* c) {
   for (DBuf* b : {&c->freq, &c->psd, &c->gamma, &c->log2rho, &c->zedge, &c->zstart, &c->zmid, &c->width,
                   &c->wlast, &c->probe_nu, &c->probe_gamma, &c->hl2, &c->rowsum, &c->counter,
                   &c->n_eval, &c->probe_g, &c->probe_quad, &c->chan_probe0, &c->eta, &c->nli_psd,
-                  &c->nli_power, &c->quad, &c->skipped, &c->batch_psd, &c->batch_report, &c->alpha, &c->aeff, &c->raman_x,
+                  &c->nli_power, &c->quad, &c->skipped, &c->batch_psd, &c->batch_report, &c->batch_ode, &c->alpha, &c->aeff, &c->raman_x,
                   &c->raman_y, &c->nf_db, &c->guard, &c->rho_end, &c->ode_work, &c->report,
                   &c->mid, &c->edge})
     b->release();
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->batch) {
+    for (cudaEvent_t ev : {c->batch->ev_start, c->batch->ev_ode[0], c->batch->ev_ode[1],
+                           c->batch->ev_nli[0], c->batch->ev_nli[1]})
+      if (ev) cudaEventDestroy(ev);
+    if (c->batch->s_ode) cudaStreamDestroy(c->batch->s_ode);
+    delete c->batch;
+    c->batch = nullptr;
+  }
   for (cudaEvent_t ev : {c->ev0, c->ev1, c->evk0, c->evk1})
     if (ev) cudaEventDestroy(ev);
   if (c->stream) cudaStreamDestroy(c->stream);

@@ -61,7 +61,12 @@ struct uwb_ctx {
   // per-channel results
   uwb::DBuf eta, nli_psd, nli_power, quad, skipped;
   // uwb_evaluate_link_many: the batch's launch profiles and reports
-  uwb::DBuf batch_psd, batch_report;
+  uwb::DBuf batch_psd, batch_report, batch_ode;
+  struct BatchState {  // overlapped uwb_evaluate_link_many (second ODE stream)
+    cudaStream_t s_ode = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_ode[2] = {nullptr, nullptr}, ev_nli[2] = {nullptr, nullptr};
+  };
+  BatchState* batch = nullptr;
   // link evaluation state (raman ODE + assembly)
   uwb::DBuf alpha, aeff, raman_x, raman_y, nf_db, guard, rho_end, ode_work, report, mid, edge;
   std::vector<int> subset;

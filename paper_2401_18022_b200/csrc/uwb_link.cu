@@ -420,8 +420,8 @@ int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_sta
 }
 
 // Report stage (assemble_link_report, link_optimizer.hpp:194-237).
-int run_report(uwb_ctx* c, cudaStream_t st) {
-  LinkDev L = c->prep->L;
+int run_report(uwb_ctx* c, cudaStream_t st, const LinkDev* Lp = nullptr) {
+  LinkDev L = Lp ? *Lp : c->prep->L;
   link_channels_kernel<<<(L.n + 127) / 128, 128, 0, st>>>(L);
   const size_t smem = static_cast<size_t>(L.n) * (3 * sizeof(double) + sizeof(int));
   static const cudaError_t attr = cudaFuncSetAttribute(
@@ -484,6 +484,17 @@ int uwb_evaluate_link_resident(uwb_ctx* c, const double* psd_dev, double* report
   return UWB_OK;
 }
 
+static int ensure_batch_state(uwb_ctx* c) {
+  if (c->batch) return UWB_OK;
+  auto* B = new uwb_ctx::BatchState();
+  cudaError_t e = cudaStreamCreateWithFlags(&B->s_ode, cudaStreamNonBlocking);
+  for (cudaEvent_t* ev : {&B->ev_start, &B->ev_ode[0], &B->ev_ode[1], &B->ev_nli[0], &B->ev_nli[1]})
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+  c->batch = B;
+  if (e != cudaSuccess) return cuda_fail(e, "batch streams");
+  return UWB_OK;
+}
+
 int uwb_evaluate_link_many(uwb_ctx* c, int n_eval, const double* psd_host, double* loss_host,
                            double* report_host) {
   if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
@@ -501,11 +512,62 @@ int uwb_evaluate_link_many(uwb_ctx* c, int n_eval, const double* psd_host, doubl
   xfer(c, d_psd, psd_host, n_eval * n * sizeof(double), cudaMemcpyHostToDevice, st);
   cudaMemsetAsync(pr->d_status, 0, sizeof(int), st);
   int launches = 0;
-  for (int e = 0; e < n_eval; ++e) {
-    int rc = run_prepared(c, d_psd + e * n, st, /*reset_status=*/false);
+  static const bool serial = [] {  // UWB_BATCH_SERIAL=1: no ODE/NLI overlap (A/B)
+    const char* e = std::getenv("UWB_BATCH_SERIAL");
+    return e && e[0] == '1';
+  }();
+  if (n_eval >= 2 && pr->P.n_probes > 0 && !serial) {
+    // Overlapped batch: the Raman ODE of evaluation e + 1 (one small CTA, on
+    // its own stream) runs while the integrand of evaluation e occupies the
+    // other SMs.  Two ODE output buffers alternate; the integrand grid leaves
+    // one SM's worth of CTAs free and the ODE uses 128 threads x <= 255
+    // registers, so it fits beside an integrand CTA.
+    int rc = ensure_batch_state(c);
     if (rc) return rc;
-    launches += c->last_launches;
-    xfer(c, d_rep + e * rl, pr->L.out, rl * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    uwb_ctx::BatchState& B = *c->batch;
+    const int per_sm = pr->grid_ctas / c->sm_count;
+    const int grid = std::max(1, pr->grid_ctas - per_sm);
+    NliParams Pb[2] = {pr->P, pr->P};
+    FinalizeParams Fb[2] = {pr->F, pr->F};
+    OdeParams Ob[2] = {pr->O, pr->O};
+    LinkDev Lb[2] = {pr->L, pr->L};
+    const size_t tab = static_cast<size_t>(n + 1) * pr->P.col_stride;
+    double* wb = c->batch_ode.get<double>(tab + 4 * n);
+    if (!wb) return fail(UWB_CUDA_ERROR, "device allocation failed");
+    cudaMemcpyAsync(wb, pr->P.log2rho, tab * sizeof(double), cudaMemcpyDeviceToDevice, st);  // pads
+    Pb[1].log2rho = wb;
+    Ob[1].log2rho = wb;
+    Ob[1].rho_end = wb + tab;
+    Lb[1].rho_end = wb + tab;
+    Ob[1].coef_a = wb + tab + n;
+    Ob[1].coef_u = wb + tab + 2 * n;
+    Ob[1].coef_v = wb + tab + 3 * n;
+    cudaEventRecord(B.ev_start, st);
+    cudaStreamWaitEvent(B.s_ode, B.ev_start, 0);  // uploads / status reset first
+    for (int e = 0; e < n_eval; ++e) {
+      const int b = e & 1;
+      const double* psd_e = d_psd + e * n;
+      Pb[b].psd = Fb[b].psd = Lb[b].psd = psd_e;
+      if (e >= 2) cudaStreamWaitEvent(B.s_ode, B.ev_nli[b], 0);  // eval e-2 done with buffer b
+      const int lo = launch_raman_ode(Ob[b], pr->P.freq, psd_e, pr->P.bch, pr->d_aeff, pr->aeff_ref,
+                                      B.s_ode, /*max_ept=*/5);
+      if (lo < 0) return fail(UWB_CUDA_ERROR, "raman ODE launch failed");
+      cudaEventRecord(B.ev_ode[b], B.s_ode);
+      cudaStreamWaitEvent(st, B.ev_ode[b], 0);
+      const int ln = launch_nli(Pb[b], Fb[b], grid, st, nullptr, nullptr);
+      if (ln < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
+      if ((rc = run_report(c, st, &Lb[b]))) return rc;
+      xfer(c, d_rep + e * rl, pr->L.out, rl * sizeof(double), cudaMemcpyDeviceToDevice, st);
+      cudaEventRecord(B.ev_nli[b], st);
+      launches += lo + ln + 2;
+    }
+  } else {
+    for (int e = 0; e < n_eval; ++e) {
+      int rc = run_prepared(c, d_psd + e * n, st, /*reset_status=*/false);
+      if (rc) return rc;
+      launches += c->last_launches;
+      xfer(c, d_rep + e * rl, pr->L.out, rl * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    }
   }
   if (loss_host) {  // the loss of each report, one strided copy
     c->d2h_bytes += n_eval * sizeof(double);
