@@ -695,10 +695,26 @@ int launch_finalize_channels_only(const FinalizeParams& f, cudaStream_t st) {
 
 namespace {
 size_t row_smem(int n_r) { return static_cast<size_t>(kWarps) * n_r * sizeof(double); }
+// static WarpSmem + dynamic row arrays may pass the 48 KB default: raise the
+// kernel's dynamic limit once per (kernel, size) high-water mark
 void allow_row_smem(RowKernel k, int n_r) {
-  if (row_smem(n_r) > 32 * 1024)
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(row_smem(n_r)));
+  static RowKernel seen_k[64];
+  static size_t seen_b[64];
+  static int n_seen = 0;
+  const size_t b = row_smem(n_r);
+  for (int i = 0; i < n_seen; ++i)
+    if (seen_k[i] == k) {
+      if (seen_b[i] >= b) return;
+      seen_b[i] = b;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b));
+      return;
+    }
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b));
+  if (n_seen < 64) {
+    seen_k[n_seen] = k;
+    seen_b[n_seen] = b;
+    ++n_seen;
+  }
 }
 }  // namespace
 

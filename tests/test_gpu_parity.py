@@ -13,7 +13,7 @@ import pytest
 
 import paper_2401_18022_b200 as uwb
 from helpers import cfg_of, engine_inputs_from_oracle, product_scenario, to_db
-from pyoracle import Case, toy_case
+from pyoracle import Case, oband11, toy_case
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -279,3 +279,24 @@ print(json.dumps({"q": np.asarray(r.quadrant).ravel().tolist(), "eta": np.asarra
     assert on["evaluated"] < 0.75 * off["evaluated"]
     assert _rel(on["q"], off["q"]) < 1e-13
     assert _rel(on["eta"], off["eta"]) < 1e-13
+
+
+@pytest.mark.parametrize("kw", [
+    dict(n_r=41),                                   # odd n_r: the middle column is its own mirror
+    dict(n_r=33, u1_uniform=1),                     # uniform u1 edges
+    dict(n_r=41, mirror_q4=0),                      # direct Q4 (not symmetric) alongside Q1/Q3
+    dict(n_r=27, span_count=2),                     # two spans: per-point z / half-log loads
+    dict(n_r=3),                                    # tiny rows
+], ids=["odd", "uniform", "direct_q4", "two_spans", "tiny"])
+def test_all_channels_nli_edge_cases_vs_oracle(kw, oracle, engine):
+    """Small edge cases against the C oracle (pinned bit-exact to the
+    reference) on identical inputs; exercises the u2-symmetric row path with
+    odd/tiny n_r, uniform u1, direct Q4 and multi-span tables."""
+    case = oband11(**kw)
+    prep = oracle.prepare(case)
+    ref = oracle.all_channels_nli(case, prep)
+    grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
+    r = uwb.all_channels_nli(grid, spans, betas, None, cfg_of(case), engine=engine, gamma=gamma)
+    assert np.array_equal(r.skipped, ref["skipped"])
+    assert _rel(r.eta, ref["eta"]) < NLI_TOL
+    assert _rel(np.asarray(r.quadrant).ravel(), np.asarray(ref["quadrant"]).ravel()) < NLI_TOL
