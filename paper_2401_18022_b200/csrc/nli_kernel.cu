@@ -59,7 +59,10 @@ struct Stencil {
 };
 
 __device__ __forceinline__ Stencil psd_and_stencil(const NliParams& P, double nu, double* psd) {
-  const double pos = (nu - P.freq[0]) / P.spacing;
+  // the reference divides; a reciprocal multiply moves pos by <= 1 ulp, which
+  // only nudges the (continuous) interpolation weight -- the PSD window test
+  // below uses nu - freq[i] itself
+  const double pos = (nu - P.freq[0]) * P.inv_spacing;
   const long i = lround(pos);
   double v = 0.0;
   if (i >= 0 && i < P.n_ch) {
@@ -465,8 +468,10 @@ __global__ void __launch_bounds__(kWarps * 32, UWB_NLI_MIN_BLOCKS) nli_rows_kern
       if (valid) {
         const double nu = S.nu, su = S.su, u1 = S.u1;
         const double u2 = S.lo + (static_cast<double>(j) + 0.5) * S.du2;
-        const double g1 = su * exp(u2);
-        const double g2 = u1 / g1;
+        // exp and the division as a 2^x table kernel and a correctly rounded
+        // reciprocal (a few ulp from the reference's libm/IEEE ops; no slow paths)
+        const double g1 = su * dev_exp2_16(u2 * (16.0 * kLog2e));
+        const double g2 = u1 * __drcp_rn(g1);
         const double f1 = S.s1 * g1;
         const double f2 = S.s2 * g2;
         double p1, p2, p3;
@@ -502,7 +507,7 @@ __global__ void __launch_bounds__(kWarps * 32, UWB_NLI_MIN_BLOCKS) nli_rows_kern
         R.w[2] = st2.hw0 * 16.0; R.w[3] = st2.hw1 * 16.0;
         R.w[4] = st3.hw0 * 16.0; R.w[5] = st3.hw1 * 16.0;
         R.phi = phi;
-        R.invphi = phi != 0.0 ? 1.0 / phi : 0.0;
+        R.invphi = phi != 0.0 ? __drcp_rn(phi) : 0.0;
         R.pw = pw;
       }
       __syncwarp();

@@ -23,6 +23,7 @@ struct NliParams {
   const double* freq;
   const double* psd;
   double spacing, bch, centre, half_band;
+  double inv_spacing;  // 1 / spacing (host): the row setup multiplies instead of dividing
   // Spans: log2(rho) tables [span][ch][lane_pos(m)] (the reference's log_rho
   // ch*steps+m scaled by log2 e so the integrand can use exp2), span-absolute
   // step geometry, all in lane order.

@@ -118,6 +118,7 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   P->freq = d_freq;
   P->psd = d_psd;
   P->spacing = g->spacing;
+  P->inv_spacing = 1.0 / g->spacing;
   P->bch = g->bch;
   P->centre = g->centre;
   P->half_band = g->half_band;

@@ -275,6 +275,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   P.freq = d_freq;
   P.psd = pr->d_psd;
   P.spacing = g->spacing;
+  P.inv_spacing = 1.0 / g->spacing;
   P.bch = g->bch;
   P.centre = g->centre;
   P.half_band = g->half_band;
