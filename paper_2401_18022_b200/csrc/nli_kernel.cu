@@ -119,9 +119,6 @@ struct WarpSmem {
 // registers (DFMA R, R, UR, R) instead of re-materialising 64-bit immediates
 // with UMOV/IMAD.MOV pairs every step, which cost v1 ~70 issue slots per step.
 __constant__ double c_e4[6] = {kE4c1, kE4c2, kE4c3, kE4c4, kE4c5, kE4c6};
-__constant__ double c_sin[6] = {kS1, kS2, kS3, kS4, kS5, kS6};
-__constant__ double c_cos[6] = {kC1, kC2, kC3, kC4, kC5, kC6};
-__constant__ double c_red[3] = {kTwoOverPi, -kPio2Hi, -kPio2Lo};
 
 // 2^(j/16) for dev_exp2_16, filled by each CTA at start.  A file-scope
 // __shared__ array (not a generic pointer) so the lookup is one LDS.
@@ -141,38 +138,6 @@ __device__ __forceinline__ double dev_exp2_16(double x) {
   p = fma(p, r, 1.0);
   const double s = s_exp2_tab[k & 15] * p;
   return __hiloint2double(__double2hiint(s) + ((k >> 4) << 20), __double2loint(s));
-}
-
-#ifndef UWB_NLI_SINCOS_TABLE
-#define UWB_NLI_SINCOS_TABLE 1
-#endif
-
-// (cos x, sin x) for |x| < 2^50 (uwb_devmath.cuh sincos_rd): 18 FP64 instructions.
-__device__ __forceinline__ void dev_sincos_quadrant(double x, double* c_out, double* s_out) {
-  const double t = fma(x, c_red[0], kMagic);
-  const int q = __double2loint(t);
-  const double kd = t - kMagic;
-  double r = fma(kd, c_red[1], x);
-  r = fma(kd, c_red[2], r);
-  const double z = r * r;
-  double ps = fma(z, c_sin[5], c_sin[4]);
-  ps = fma(ps, z, c_sin[3]);
-  ps = fma(ps, z, c_sin[2]);
-  ps = fma(ps, z, c_sin[1]);
-  ps = fma(ps, z, c_sin[0]);
-  const double s = fma(r * z, ps, r);
-  double pc = fma(z, c_cos[5], c_cos[4]);
-  pc = fma(pc, z, c_cos[3]);
-  pc = fma(pc, z, c_cos[2]);
-  pc = fma(pc, z, c_cos[1]);
-  pc = fma(pc, z, c_cos[0]);
-  pc = fma(pc, z, -0.5);
-  const double c = fma(pc, z, 1.0);
-  const bool swap = (q & 1) != 0;
-  const double so = swap ? c : s;
-  const double co = swap ? s : c;
-  *s_out = __hiloint2double(__double2hiint(so) ^ ((q & 2) << 30), __double2loint(so));
-  *c_out = __hiloint2double(__double2hiint(co) ^ (((q + 1) & 2) << 30), __double2loint(co));
 }
 
 // (cos x, sin x) for |x| < 2^50 by a 16-entry full-circle table: x = k pi/8
@@ -211,11 +176,7 @@ __device__ __forceinline__ void dev_sincos_table(double x, double* c_out, double
 }
 
 __device__ __forceinline__ void dev_sincos(double x, double* c_out, double* s_out) {
-#if UWB_NLI_SINCOS_TABLE
   dev_sincos_table(x, c_out, s_out);
-#else
-  dev_sincos_quadrant(x, c_out, s_out);
-#endif
 }
 
 // |sum over spans & steps|^2 for one point, computed by one 16-lane segment.

@@ -277,4 +277,28 @@ constexpr double kC16c4 = -0.0000002753720453432431172966888;
    -0.38268343236508978, -0.70710678118654757, -0.92387953251128674, -1.0,                  \
    -0.92387953251128674, -0.70710678118654757, -0.38268343236508978}
 
+// Host/device restatement of the integrand's sincos (nli_kernel.cu
+// dev_sincos_table): x = k pi/8 + r by Cody-Waite, minimax kernels on r, then
+// the angle addition with cos/sin(k pi/8).  Tested against long double libm.
+UWB_HD void sincos_tab16(double x, const double* cos16, const double* sin16, double* c_out,
+                         double* s_out) {
+  const double t = fmad(x, kEightOverPi, kMagic);
+  const int q = lo_word(t) & 15;
+  const double kd = t - kMagic;
+  double r = fmad(kd, -kPio8Hi, x);
+  r = fmad(kd, -kPio8Lo, r);
+  const double z = r * r;
+  double ps = fmad(z, kS16c4, kS16c3);
+  ps = fmad(ps, z, kS16c2);
+  ps = fmad(ps, z, kS16c1);
+  const double sr = fmad(r * z, ps, r);
+  double pc = fmad(z, kC16c4, kC16c3);
+  pc = fmad(pc, z, kC16c2);
+  pc = fmad(pc, z, kC16c1);
+  pc = fmad(pc, z, kC16c0);
+  const double cr = fmad(pc, z, 1.0);
+  *c_out = fmad(cos16[q], cr, -(sin16[q] * sr));
+  *s_out = fmad(sin16[q], cr, cos16[q] * sr);
+}
+
 }  // namespace uwb
