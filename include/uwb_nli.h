@@ -221,6 +221,18 @@ int uwb_last_ode_stats(uwb_ctx* ctx, double* ode_ms, long long* rhs_evals);
 int uwb_last_transfer_bytes(uwb_ctx* ctx, unsigned long long* h2d, unsigned long long* d2h);
 /* Live FP64 FMA-pipe peak of this device, TFLOP/s (roofline denominator). */
 int uwb_fp64_peak(uwb_ctx* ctx, double* tflops);
+/* Step arithmetic of the NLI integrand for subsequent calls (and for
+ * subsequent uwb_evaluate_link_prepare; a prepared link keeps its mode).
+ * UWB_PRECISION_FP64 (default): every operation in FP64, the reference's
+ * arithmetic.  UWB_PRECISION_MIXED: compensated FP32 -- the log2-rho
+ * interpolation, the phase and its reduction, and all sums past a lane stay
+ * FP64; 2^x, sin/cos and the lane's partial sums of reduced, well-conditioned
+ * arguments run in FP32 (BASELINE config 4, "FP64 vs compensated FP32";
+ * accuracy per setting in profiles/r01_config4_sweep.json).  This is an
+ * extension: the reference has no precision knob. */
+#define UWB_PRECISION_FP64 0
+#define UWB_PRECISION_MIXED 1
+int uwb_set_precision(uwb_ctx* ctx, int mode);
 /* Kernel launches issued by the last call (evidence for bench gpu_launches). */
 int uwb_last_launch_count(uwb_ctx* ctx);
 /* Device time (ms) of the last NLI integrand kernel and its inner-step count

@@ -20,7 +20,7 @@ OUT = os.path.join(PKG, "libuwbnli.so")
 SOURCES = ["nli_kernel.cu", "raman_ode.cu", "uwb_capi.cu", "uwb_link.cu", "uwb_model.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-         "-shared", "-Xptxas", "-warn-spills"]
+         "-Xptxas", "-warn-spills"]
 
 
 def nvcc():
@@ -39,18 +39,43 @@ def needs_build():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+def compile_link(out, extra=(), verbose=False):
+    """One nvcc -c per source in parallel (the template instantiations make
+    each file slow on its own), then one shared-library link."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    objs = [out + "." + os.path.splitext(src)[0] + ".o" for src in SOURCES]
+
+    def cc(args):
+        src, obj = args
+        cmd = [nvcc()] + ARCH + FLAGS + list(extra) + ["-c", "-o", obj, os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        return subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        results = list(ex.map(cc, zip(SOURCES, objs)))
+    link = [nvcc()] + ARCH + ["-shared", "-o", out] + objs
+    results.append(subprocess.run(link, capture_output=True, text=True)
+                   if all(r.returncode == 0 for r in results) else None)
+    for o in objs:
+        if os.path.exists(o):
+            os.remove(o)
+    for r in results:
+        if r is None:
+            continue
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed")
+        if verbose and (r.stdout or r.stderr):
+            sys.stderr.write(r.stdout + r.stderr)
+    return out
+
+
 def build(verbose=False, force=False):
     if not force and not needs_build():
         return OUT
-    cmd = [nvcc()] + ARCH + FLAGS + ["-o", OUT + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed")
-    if verbose and (r.stdout or r.stderr):
-        sys.stderr.write(r.stdout + r.stderr)
+    compile_link(OUT + ".tmp", verbose=verbose)
     os.replace(OUT + ".tmp", OUT)
     return OUT
 

@@ -179,6 +179,69 @@ __device__ __forceinline__ void dev_sincos(double x, double* c_out, double* s_ou
   dev_sincos_table(x, c_out, s_out);
 }
 
+// ---- compensated-FP32 ("mixed") step arithmetic (GnSolverConfig precision
+// extension, BASELINE config 4).  What must stay FP64 stays FP64: the log2 rho
+// interpolation, the split of 16 log2 p into (k, r), the phase phi z and its
+// reduction modulo pi/8, and every sum past the lane.  What is evaluated in
+// FP32 is only what is already small and well conditioned: 2^(r/16) on
+// |r| <= 1/2, sin/cos on |r| <= pi/16, expm1 of the step-to-step log change,
+// and the lane's K-step partial sums.  The summation-by-parts differences
+// p_{m-1} - p_m are formed as p_m (2^(d/16) - 1) with d = lg_{m-1} - lg_m
+// taken in FP64 first, so they never cancel in FP32.
+__shared__ float s_exp2_tabf[16];
+__shared__ float s_cos16f[16];
+__shared__ float s_sin16f[16];
+
+// 2^(x/16) for x = 16 log2 p in FP64 -> FP32 (relative error ~1e-7).
+__device__ __forceinline__ float mixed_exp2_16(double x) {
+  const double t = x + kMagic;
+  int k = __double2loint(t);
+  const float r = __double2float_rn(x - (t - kMagic));  // |r| <= 1/2
+  const float y = r * 0.043321698784996581f;            // r ln2 / 16
+  float e = fmaf(y, 1.0f / 24.0f, 1.0f / 6.0f);
+  e = fmaf(e, y, 0.5f);
+  e = fmaf(e, y, 1.0f);
+  e = fmaf(e, y, 1.0f);
+  k = max(k, -16 * 120);  // p < 2^-120 is far below anything the sum resolves
+  const float v = s_exp2_tabf[k & 15] * e;
+  return __int_as_float(__float_as_int(v) + ((k >> 4) << 23));
+}
+
+// p_m (2^(d/16) - 1) = p_{m-1} - p_m without cancellation: Taylor in
+// y = d ln2/16 for |y| < 0.3 (relative error < 1e-8); past that the plain
+// difference loses at most two bits.
+__device__ __forceinline__ float mixed_dp(float p, float pprev, float d) {
+  const float y = d * 0.043321698784996581f;
+  float e = fmaf(y, 1.0f / 5040.0f, 1.0f / 720.0f);
+  e = fmaf(e, y, 1.0f / 120.0f);
+  e = fmaf(e, y, 1.0f / 24.0f);
+  e = fmaf(e, y, 1.0f / 6.0f);
+  e = fmaf(e, y, 0.5f);
+  e = fmaf(e, y, 1.0f);
+  return fabsf(y) < 0.3f ? p * (e * y) : pprev - p;
+}
+
+// (cos x, sin x) in FP32 with the reduction x = k pi/8 + r done in FP64 (the
+// phase reaches 1e5 rad), r rounded to FP32 (|r| <= pi/16), Taylor kernels
+// (sin to r^5, cos to r^6: truncation < 3e-9) and the 16-entry tables.
+__device__ __forceinline__ void mixed_sincos(double x, float* c_out, float* s_out) {
+  const double t = fma(x, c_red8[0], kMagic);
+  const int q = __double2loint(t) & 15;
+  const double kd = t - kMagic;
+  double rd = fma(kd, c_red8[1], x);
+  rd = fma(kd, c_red8[2], rd);
+  const float r = __double2float_rn(rd);
+  const float z = r * r;
+  const float ps = fmaf(z, 1.0f / 120.0f, -1.0f / 6.0f);
+  const float sr = fmaf(r * z, ps, r);
+  float pc = fmaf(z, -1.0f / 720.0f, 1.0f / 24.0f);
+  pc = fmaf(pc, z, -0.5f);
+  const float cr = fmaf(pc, z, 1.0f);
+  const float tc = s_cos16f[q], ts = s_sin16f[q];
+  *c_out = fmaf(tc, cr, -(ts * sr));
+  *s_out = fmaf(ts, cr, tc * sr);
+}
+
 // |sum over spans & steps|^2 for one point, computed by one 16-lane segment.
 // Lane sl owns the K consecutive steps m = sl K + b (lane_pos layout, so for
 // each b the segment's 16 loads of a column are one 128-byte line).
@@ -310,7 +373,136 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
   return re * re + im * im;
 }
 
+// point_kernel in compensated FP32 (see mixed_exp2_16 above): same lane
+// layout, same summation by parts, same fast/slow split; lane partial sums in
+// FP32, everything across lanes in FP64.
 template <int K, bool FULL, bool HOIST>
+__device__ __forceinline__ double point_kernel_mixed(const NliParams& P, const WarpSmem& S, int idx,
+                                                     int probe, int sl, unsigned segmask,
+                                                     const double (&Zr)[K], const double (&Hr)[K]) {
+  constexpr int NS = 16 * K;
+  const int N = P.steps;
+  const PointRec& R = S.pt[idx];
+  const double2 wa = *reinterpret_cast<const double2*>(&R.w[0]);
+  const double2 wb = *reinterpret_cast<const double2*>(&R.w[2]);
+  const double2 wc = *reinterpret_cast<const double2*>(&R.w[4]);
+  const double2 ph = *reinterpret_cast<const double2*>(&R.phi);
+  const int4 cl = *reinterpret_cast<const int4*>(&R.col[0]);
+  const double phi = ph.x;
+  const double w0 = wa.x, w1 = wa.y, w2 = wb.x, w3 = wb.y, w4 = wc.x, w5 = wc.y;
+  const int oa = cl.x + sl, ob = cl.y + sl, oc = cl.z + sl;
+  double fre = 0.0, fim = 0.0, sre = 0.0, sim = 0.0;
+  const int n_spans = HOIST ? 1 : P.n_spans;
+  for (int k = 0; k < n_spans; ++k) {
+    const double* T = P.log2rho + k * P.span_stride;
+    const double* ca = T + oa;
+    const double* cb = T + ob;
+    const double* cc3 = T + oc;
+    const double* hl = P.hl2 + (static_cast<size_t>(probe) * P.n_spans + k) * NS + sl;
+    const bool fast = fabs(phi) * __ldg(P.wlast + k) > 1e-4;
+    if (fast) {
+      const double* ze = P.zedge + static_cast<size_t>(k) * NS + sl;
+      float lre = 0.0f, lim = 0.0f;
+      float p0 = 0.0f, pp = 0.0f, pc = 0.0f, ps = 0.0f;
+      double lg0 = 0.0, lgp = 0.0;
+#pragma unroll
+      for (int b = 0; b < K; ++b) {
+        const int o = 16 * b;
+        const double H = HOIST ? Hr[b] : __ldg(hl + o);
+        const double Z = HOIST ? Zr[b] : __ldg(ze + o);
+        double lg = fma(w0, __ldg(ca + o), -H);
+        lg = fma(w1, __ldg(ca + NS + o), lg);
+        lg = fma(w2, __ldg(cb + o), lg);
+        lg = fma(w3, __ldg(cb + NS + o), lg);
+        lg = fma(w4, __ldg(cc3 + o), lg);
+        lg = fma(w5, __ldg(cc3 + NS + o), lg);
+        float p = mixed_exp2_16(lg);
+        double ang = phi * Z;
+        const bool ok = FULL || sl * K + b < N;
+        if (!FULL) {
+          p = ok ? p : 0.0f;
+          ang = ok ? ang : 0.0;
+        }
+        float cs, sn;
+        mixed_sincos(ang, &cs, &sn);
+        if (b == 0) {
+          p0 = p;
+          lg0 = lg;
+        } else {  // (p_{m-1} - p_m) E_m = p_m (2^((lg_{m-1} - lg_m)/16) - 1) E_m
+          float cf = mixed_dp(p, pp, __double2float_rn(lgp - lg));
+          if (!FULL) cf = ok ? cf : pp;
+          lre = fmaf(cf, pc, lre);
+          lim = fmaf(cf, ps, lim);
+        }
+        pp = p;
+        lgp = lg;
+        pc = cs;
+        ps = sn;
+      }
+      // the lane's last step pairs with the next lane's first (p_N = 0)
+      float pn = __shfl_down_sync(segmask, p0, 1, 16);
+      const double lgn = __shfl_down_sync(segmask, lg0, 1, 16);
+      if (sl == 15) pn = 0.0f;
+      const float cf = pn == 0.0f ? pp : mixed_dp(pn, pp, __double2float_rn(lgp - lgn));
+      lre = fmaf(cf, pc, lre);
+      lim = fmaf(cf, ps, lim);
+      fre += static_cast<double>(lre);
+      fim += static_cast<double>(lim);
+      // -p_0 E(z_0): E = 1 when the span starts at z = 0
+      const double z0 = __ldg(P.zstart + k);
+      if (z0 == 0.0) {
+        if (sl == 0) fre -= p0;
+      } else {
+        double c0v, s0v;
+        dev_sincos(phi * z0, &c0v, &s0v);
+        if (sl == 0) {
+          fre = fma(-static_cast<double>(p0), c0v, fre);
+          fim = fma(-static_cast<double>(p0), s0v, fim);
+        }
+      }
+    } else {
+      const double* zm = P.zmid + static_cast<size_t>(k) * NS + sl;
+      const double* wd = P.width + static_cast<size_t>(k) * NS + sl;
+      float lre = 0.0f, lim = 0.0f;
+      const float phf = static_cast<float>(phi);
+#pragma unroll
+      for (int b = 0; b < K; ++b) {
+        const int o = 16 * b;
+        const double H = HOIST ? Hr[b] : __ldg(hl + o);
+        double lg = fma(w0, __ldg(ca + o), -H);
+        lg = fma(w1, __ldg(ca + NS + o), lg);
+        lg = fma(w2, __ldg(cb + o), lg);
+        lg = fma(w3, __ldg(cb + NS + o), lg);
+        lg = fma(w4, __ldg(cc3 + o), lg);
+        lg = fma(w5, __ldg(cc3 + NS + o), lg);
+        const float p = mixed_exp2_16(lg);
+        const float wm = static_cast<float>(__ldg(wd + o));
+        // |x| = |phi| w / 2 <= 5e-5: 1 - x^2/6 is exact in FP32
+        const float x = 0.5f * phf * wm;
+        const float sinc = fmaf(x * x, -1.0f / 6.0f, 1.0f);
+        float w = p * wm * sinc;
+        if (!FULL) w = (sl * K + b < N) ? w : 0.0f;
+        float cs, sn;
+        mixed_sincos(phi * __ldg(zm + o), &cs, &sn);
+        lre = fmaf(w, cs, lre);
+        lim = fmaf(w, sn, lim);
+      }
+      sre += static_cast<double>(lre);
+      sim += static_cast<double>(lim);
+    }
+  }
+  const double invphi = ph.y;
+  double re = fma(fim, invphi, sre);
+  double im = fma(-fre, invphi, sim);
+#pragma unroll
+  for (int o = 8; o >= 1; o >>= 1) {
+    re += __shfl_xor_sync(segmask, re, o, 16);
+    im += __shfl_xor_sync(segmask, im, o, 16);
+  }
+  return re * re + im * im;
+}
+
+template <int K, bool FULL, bool HOIST, bool MIXED>
 __global__ void __launch_bounds__(kWarps * 32, UWB_NLI_MIN_BLOCKS) nli_rows_kernel(const NliParams P) {
   __shared__ WarpSmem s_w[kWarps];
   extern __shared__ double row_vals[];  // [kWarps][n_r]
@@ -318,6 +510,11 @@ __global__ void __launch_bounds__(kWarps * 32, UWB_NLI_MIN_BLOCKS) nli_rows_kern
     s_exp2_tab[threadIdx.x] = c_exp2_tab16[threadIdx.x];
     s_cos16[threadIdx.x] = c_tab_cos16[threadIdx.x];
     s_sin16[threadIdx.x] = c_tab_sin16[threadIdx.x];
+    if (MIXED) {
+      s_exp2_tabf[threadIdx.x] = __double2float_rn(c_exp2_tab16[threadIdx.x]);
+      s_cos16f[threadIdx.x] = __double2float_rn(c_tab_cos16[threadIdx.x]);
+      s_sin16f[threadIdx.x] = __double2float_rn(c_tab_sin16[threadIdx.x]);
+    }
   }
   __syncthreads();
 
@@ -480,7 +677,9 @@ __global__ void __launch_bounds__(kWarps * 32, UWB_NLI_MIN_BLOCKS) nli_rows_kern
       for (int base = 0; base < n_need; base += 2) {
         const bool ok = base + seg < n_need;
         const int idx = ok ? base + seg : base;
-        const double kv = point_kernel<K, FULL, HOIST>(P, S, idx, probe, sl, segmask, Zr, Hr);
+        const double kv =
+            MIXED ? point_kernel_mixed<K, FULL, HOIST>(P, S, idx, probe, sl, segmask, Zr, Hr)
+                  : point_kernel<K, FULL, HOIST>(P, S, idx, probe, sl, segmask, Zr, Hr);
         if (ok && sl == 0) S.kv[S.pt[idx].src] = kv;
       }
       __syncwarp();
@@ -581,32 +780,39 @@ __global__ void finalize_channels_kernel(const FinalizeParams F) {
 
 using RowKernel = void (*)(const NliParams);
 
-template <int K>
-RowKernel pick(int steps, bool one_span) {
+template <int K, bool MIXED>
+RowKernel pick2(int steps, bool one_span) {
   constexpr bool kHoist = K <= 8;
   if (one_span && kHoist)
-    return steps == 16 * K ? nli_rows_kernel<K, true, kHoist> : nli_rows_kernel<K, false, kHoist>;
-  return steps == 16 * K ? nli_rows_kernel<K, true, false> : nli_rows_kernel<K, false, false>;
+    return steps == 16 * K ? nli_rows_kernel<K, true, kHoist, MIXED>
+                           : nli_rows_kernel<K, false, kHoist, MIXED>;
+  return steps == 16 * K ? nli_rows_kernel<K, true, false, MIXED>
+                         : nli_rows_kernel<K, false, false, MIXED>;
 }
 
-RowKernel row_kernel_for(int steps, bool one_span) {
+template <int K>
+RowKernel pick(int steps, bool one_span, bool mixed) {
+  return mixed ? pick2<K, true>(steps, one_span) : pick2<K, false>(steps, one_span);
+}
+
+RowKernel row_kernel_for(int steps, bool one_span, bool mixed) {
   switch ((steps + 15) / 16) {
-    case 1: return pick<1>(steps, one_span);
-    case 2: return pick<2>(steps, one_span);
-    case 3: return pick<3>(steps, one_span);
-    case 4: return pick<4>(steps, one_span);
-    case 5: return pick<5>(steps, one_span);
-    case 6: return pick<6>(steps, one_span);
-    case 7: return pick<7>(steps, one_span);
-    case 8: return pick<8>(steps, one_span);
-    case 9: return pick<9>(steps, one_span);
-    case 10: return pick<10>(steps, one_span);
-    case 11: return pick<11>(steps, one_span);
-    case 12: return pick<12>(steps, one_span);
-    case 13: return pick<13>(steps, one_span);
-    case 14: return pick<14>(steps, one_span);
-    case 15: return pick<15>(steps, one_span);
-    case 16: return pick<16>(steps, one_span);
+    case 1: return pick<1>(steps, one_span, mixed);
+    case 2: return pick<2>(steps, one_span, mixed);
+    case 3: return pick<3>(steps, one_span, mixed);
+    case 4: return pick<4>(steps, one_span, mixed);
+    case 5: return pick<5>(steps, one_span, mixed);
+    case 6: return pick<6>(steps, one_span, mixed);
+    case 7: return pick<7>(steps, one_span, mixed);
+    case 8: return pick<8>(steps, one_span, mixed);
+    case 9: return pick<9>(steps, one_span, mixed);
+    case 10: return pick<10>(steps, one_span, mixed);
+    case 11: return pick<11>(steps, one_span, mixed);
+    case 12: return pick<12>(steps, one_span, mixed);
+    case 13: return pick<13>(steps, one_span, mixed);
+    case 14: return pick<14>(steps, one_span, mixed);
+    case 15: return pick<15>(steps, one_span, mixed);
+    case 16: return pick<16>(steps, one_span, mixed);
     default: return nullptr;
   }
 }
@@ -684,8 +890,8 @@ void allow_row_smem(RowKernel k, int n_r) {
 }
 }  // namespace
 
-int nli_ctas_per_sm(int steps, bool one_span, int n_r) {
-  RowKernel k = row_kernel_for(steps, one_span);
+int nli_ctas_per_sm(int steps, bool one_span, int n_r, bool mixed) {
+  RowKernel k = row_kernel_for(steps, one_span, mixed);
   if (!k) return 0;
   allow_row_smem(k, n_r);
   int n = 0;
@@ -701,7 +907,7 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
     const char* e = std::getenv("UWB_NLI_NO_HOIST");
     return e && e[0] == '1';
   }();
-  RowKernel k = row_kernel_for(p.steps, p.n_spans == 1 && !no_hoist);
+  RowKernel k = row_kernel_for(p.steps, p.n_spans == 1 && !no_hoist, p.mixed != 0);
   if (!k || p.n_probes <= 0 || p.col_stride != 16 * ((p.steps + 15) / 16)) return -1;
   int launches = 0;
   cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), stream);

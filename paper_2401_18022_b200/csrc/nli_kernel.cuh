@@ -53,6 +53,7 @@ struct NliParams {
   unsigned long long* n_eval;   // [2]: |K|^2 evaluations, active points (stats)
   unsigned long long* n_active; // = n_eval + 1
   int mirror_u2;                // share |K|^2 across u2 -> -u2 in symmetric rows
+  int mixed;                    // 1: compensated-FP32 step arithmetic (uwb_set_precision)
   double* rowsum;               // [total_rows]; NaN => row not added (reference `continue`)
 };
 
@@ -107,7 +108,7 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
                cudaEvent_t ev_k0, cudaEvent_t ev_k1);
 
 // CTAs per SM the integrand kernel reaches for a given step count.
-int nli_ctas_per_sm(int steps, bool one_span, int n_r);
+int nli_ctas_per_sm(int steps, bool one_span, int n_r, bool mixed = false);
 constexpr int kMaxSteps = 256;  // 16 lanes x 16 steps per lane
 // Elements allocated past the end of log2rho / zedge / hl2: the integrand's
 // lanes with m >= N load them and mask the result (branch-free tail).

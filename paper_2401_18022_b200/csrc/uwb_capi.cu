@@ -140,7 +140,7 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   return UWB_OK;
 }
 
-int set_cfg(const uwb_nli_cfg* cfg, NliParams* P) {
+int set_cfg(const uwb_nli_cfg* cfg, NliParams* P, int precision) {
   if (!cfg) return fail(UWB_CONFIG_ERROR, "missing solver config");
   if (cfg->n_r < 2) return fail(UWB_CONFIG_ERROR, "nli_psd_at: n_r must be >= 2");
   P->n_r = cfg->n_r;
@@ -153,6 +153,7 @@ int set_cfg(const uwb_nli_cfg* cfg, NliParams* P) {
     return e && e[0] == '1';
   }();
   P->mirror_u2 = no_mirror ? 0 : 1;
+  P->mixed = precision == UWB_PRECISION_MIXED ? 1 : 0;
   return UWB_OK;
 }
 
@@ -213,7 +214,7 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
   }
   cudaEventRecord(c->ev0, st);
   if (np) {
-    const int per_sm = nli_ctas_per_sm(P.steps, P.n_spans == 1, P.n_r);
+    const int per_sm = nli_ctas_per_sm(P.steps, P.n_spans == 1, P.n_r, P.mixed != 0);
     if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
     const int launched = launch_nli(P, F, c->sm_count * per_sm, st, c->evk0, c->evk1);
     if (launched < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
@@ -376,7 +377,7 @@ int uwb_all_channels_nli(uwb_ctx* c, const uwb_grid* grid, int n_spans, const uw
   int rc = validate_grid(grid);
   if (rc) return rc;
   NliParams P{};
-  if ((rc = set_cfg(cfg, &P))) return rc;
+  if ((rc = set_cfg(cfg, &P, c->precision))) return rc;
   if (!gamma) return set_err(UWB_CONFIG_ERROR, "missing per-channel gamma");
   std::vector<double> nu, gam;
   std::vector<int> cp;
@@ -427,7 +428,7 @@ int uwb_nli_psd_at(uwb_ctx* c, const uwb_grid* grid, int n_spans, const uwb_span
   if (rc) return rc;
   NliParams P{};
   if ((rc = upload_path_inputs(c, grid, n_spans, spans, beta, &P))) return rc;
-  if ((rc = set_cfg(cfg, &P))) return rc;
+  if ((rc = set_cfg(cfg, &P, c->precision))) return rc;
   if (n_probe <= 0) return UWB_OK;
   std::vector<double> vnu(nu, nu + n_probe), vg(gamma, gamma + n_probe);
   if ((rc = run_probes(c, P, cfg, vnu, vg, nullptr, true))) return rc;
@@ -496,6 +497,14 @@ int uwb_last_transfer_bytes(uwb_ctx* c, unsigned long long* h2d, unsigned long l
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
   if (h2d) *h2d = c->h2d_bytes;
   if (d2h) *d2h = c->d2h_bytes;
+  return UWB_OK;
+}
+
+int uwb_set_precision(uwb_ctx* c, int mode) {
+  if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  if (mode != UWB_PRECISION_FP64 && mode != UWB_PRECISION_MIXED)
+    return set_err(UWB_CONFIG_ERROR, "uwb_set_precision: unknown mode");
+  c->precision = mode;
   return UWB_OK;
 }
 

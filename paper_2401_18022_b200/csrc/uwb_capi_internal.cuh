@@ -31,7 +31,7 @@ inline cudaError_t xfer_sync(uwb_ctx* c, void* dst, const void* src, size_t byte
 inline void reset_xfer(uwb_ctx* c) { c->h2d_bytes = c->d2h_bytes = 0; }
 int cuda_fail(cudaError_t e, const char* what);
 int validate_grid(const uwb_grid* g);
-int set_cfg(const uwb_nli_cfg* cfg, NliParams* P);
+int set_cfg(const uwb_nli_cfg* cfg, NliParams* P, int precision);
 int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vector<double>& nu,
                const std::vector<double>& gam, const std::vector<int>* chan_probe0,
                bool sync_stats);

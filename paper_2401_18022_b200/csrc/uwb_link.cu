@@ -248,7 +248,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   pr->length = fb->length_m;
   pr->cfg = *cfg;
   NliParams& P = pr->P;
-  if ((rc = set_cfg(cfg, &P))) return rc;
+  if ((rc = set_cfg(cfg, &P, c->precision))) return rc;
 
   // static uploads
   const double* d_freq = up(c, c->freq, g->freq, n);
@@ -382,7 +382,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   L.out = c->report.get<double>(4 * static_cast<size_t>(n) + 3 + 2 * L.n_bands);
   L.tmp = d_tmp;
 
-  const int per_sm = nli_ctas_per_sm(steps, P.n_spans == 1, P.n_r);
+  const int per_sm = nli_ctas_per_sm(steps, P.n_spans == 1, P.n_r, P.mixed != 0);
   if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
   pr->grid_ctas = c->sm_count * per_sm;
   cudaError_t e = cudaStreamSynchronize(c->stream);

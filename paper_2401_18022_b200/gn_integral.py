@@ -288,6 +288,17 @@ class Engine:
         N.check(self.lib.uwb_last_transfer_bytes(self.h, N.C.byref(a), N.C.byref(b)))
         return a.value, b.value
 
+    def set_precision(self, mode: str):
+        """Integrand step arithmetic for subsequent calls: "fp64" (default,
+        the reference's arithmetic) or "mixed" (compensated FP32; see
+        include/uwb_nli.h uwb_set_precision).  An extension: the reference
+        has no such knob."""
+        modes = {"fp64": 0, "mixed": 1}
+        if mode not in modes:
+            raise ConfigError(f"set_precision: unknown mode {mode!r}")
+        N.check(self.lib.uwb_set_precision(self.h, modes[mode]))
+        self.precision = mode
+
     def fp64_peak_tflops(self):
         t = N.C.c_double()
         N.check(self.lib.uwb_fp64_peak(self.h, N.C.byref(t)))

@@ -300,3 +300,50 @@ def test_all_channels_nli_edge_cases_vs_oracle(kw, oracle, engine):
     assert np.array_equal(r.skipped, ref["skipped"])
     assert _rel(r.eta, ref["eta"]) < NLI_TOL
     assert _rel(np.asarray(r.quadrant).ravel(), np.asarray(ref["quadrant"]).ravel()) < NLI_TOL
+
+
+# ---------------------------------------------------------------- compensated FP32 ("mixed")
+MIXED_TOL = 1e-6  # north_star: <= 1e-6 relative eta (the FP64 path meets 1e-9)
+
+
+@pytest.fixture
+def mixed_engine(engine):
+    engine.set_precision("mixed")
+    yield engine
+    engine.set_precision("fp64")
+
+
+@pytest.mark.parametrize("name", ["cband11", "oband11", "oband11_simpson", "toy3_3span",
+                                  "cband11_nr40", "uwb589_75_0.95", "uwb589_150_1.4"])
+def test_mixed_precision_nli_within_tolerance(name, golden, oracle, mixed_engine):
+    """BASELINE config 4's compensated-FP32 column: the mixed integrand stays
+    within the north-star tolerance of the reference on the golden cases
+    (observed <= 5e-8)."""
+    rec = golden["all_channels_nli"][name]
+    case = Case.from_json(rec["case"])
+    prep = oracle.prepare(case)
+    grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
+    r = uwb.all_channels_nli(grid, spans, betas, None, cfg_of(case), engine=mixed_engine,
+                             gamma=gamma)
+    assert np.array_equal(r.skipped, np.array(rec["skipped"], np.uint8))
+    eta = np.array(rec["eta"])
+    act = eta > 0
+    assert _rel(r.eta[act], eta[act]) < MIXED_TOL
+    assert np.max(np.abs(to_db(r.eta[act]) - to_db(eta[act]))) < 0.01
+
+
+def test_mixed_precision_evaluate_link(golden, mixed_engine):
+    rec = golden["evaluate_link"]["uwb589_random_launch"]
+    case = Case.from_json(rec["case"])
+    grid, fibre = product_scenario(case)
+    lc = uwb.LinkConfig(gn=cfg_of(case), raman=uwb.RamanSolveOptions(bool(case.raman)))
+    rep = uwb.evaluate_link(fibre, grid, lc, engine=mixed_engine)
+    eta_ref = np.array(rec["eta"])
+    act = eta_ref > 0
+    assert _rel(rep.eta[act], eta_ref[act]) < MIXED_TOL
+    assert np.max(np.abs(rep.snr_db[act] - np.array(rec["snr_db"])[act])) < 0.01
+
+
+def test_precision_mode_errors(engine):
+    with pytest.raises(uwb.ConfigError):
+        engine.set_precision("fp16")

@@ -15,9 +15,8 @@ name, defs = sys.argv[1], sys.argv[2:]
 out_dir = os.path.join(ROOT, "scratch", "v")
 os.makedirs(out_dir, exist_ok=True)
 out = os.path.join(out_dir, name + ".so")
-cmd = [b.nvcc()] + b.ARCH + b.FLAGS + defs + ["-o", out] + [os.path.join(b.CSRC, s) for s in b.SOURCES]
-r = subprocess.run(cmd, capture_output=True, text=True)
-if r.returncode:
-    sys.stderr.write(r.stdout + r.stderr)
+try:
+    b.compile_link(out, extra=defs)
+except RuntimeError:
     sys.exit(1)
 print(out)

@@ -17,8 +17,10 @@ p = argparse.ArgumentParser()
 p.add_argument("--n-r", type=int, default=150)
 p.add_argument("--density", type=float, default=1.4)
 p.add_argument("--iters", type=int, default=3)
+p.add_argument("--precision", default="fp64", choices=["fp64", "mixed"])
 a = p.parse_args()
 eng = uwb.Engine(0)
+eng.set_precision(a.precision)
 grid = uwb.make_default_uwb_grid()
 uwb.set_uniform_launch(grid, 1e-3)
 res = uwb.ResidentLink(uwb.default_fibre(), grid,
