@@ -13,6 +13,7 @@
  *   uwb_channel_nli        <- uwblink::channel_nli        gn_integral.hpp:316-320
  *   uwb_power_evolution    <- uwblink::solve_power_evolution raman_power.hpp:52-55
  *   uwb_evaluate_link      <- uwblink::evaluate_link      link_optimizer.hpp:241-245
+ *   uwb_cfm_all_channels_nli <- uwblink::cfm_all_channels_nli gn_closed_form.hpp:70-74
  *                              (= solve_link_noise :181-190 + assemble_link_report :194-237)
  *
  * Conventions
@@ -157,6 +158,14 @@ int uwb_set_channel_subset(uwb_ctx* ctx, int n, const int* channels);
 int uwb_all_channels_nli(uwb_ctx* ctx, const uwb_grid* grid, int n_spans, const uwb_span* spans,
                          const double beta[3], const double* gamma, const uwb_nli_cfg* cfg,
                          uwb_nli_result* out);
+
+/* cfm_all_channels_nli (gn_closed_form.hpp:70-144): the closed-form SPM +
+ * XPM model over the same inputs (gamma[n_ch] = gamma_at per channel, :84-87;
+ * spans may differ in step count).  quadrant (if non-NULL) is zeroed like
+ * the reference's; elapsed_seconds is device time. */
+int uwb_cfm_all_channels_nli(uwb_ctx* ctx, const uwb_grid* grid, int n_spans,
+                             const uwb_span* spans, const double beta[3], const double* gamma,
+                             uwb_nli_result* out);
 
 /* nli_psd_at (gn_integral.hpp:218-313) for n_probe absolute probe frequencies
  * with per-probe gamma; quadrant4 [n_probe*4] may be NULL. */

@@ -239,6 +239,16 @@ class RefLib:
         return dict(eta=eta, nli_psd=psd, nli_power=pw, quadrant=q.reshape(n, 4), skipped=sk,
                     nli_seconds=tn.value, ode_seconds=to.value)
 
+    def cfm_all_channels_nli(self, case):
+        """cfm_all_channels_nli (gn_closed_form.hpp:70) after the reference ODE."""
+        n = 589 if case.uwb_default else case.n_ch
+        eta, psd, pw = np.zeros(n), np.zeros(n), np.zeros(n)
+        sk = np.zeros(n, np.uint8)
+        t = C.c_double()
+        self._chk(self.lib.ref_cfm_all_channels_nli(C.byref(self._rc(case)), _dp(eta), _dp(psd),
+                                                    _dp(pw), _u8(sk), C.byref(t)))
+        return dict(eta=eta, nli_psd=psd, nli_power=pw, skipped=sk, seconds=t.value)
+
     def nli_psd_at(self, case, gamma, nu):
         q = np.zeros(4)
         out = C.c_double()
@@ -458,6 +468,20 @@ class Oracle:
                                                _dp(gam), C.byref(cfg), _dp(eta), _dp(psd),
                                                _dp(pw), _dp(q), _u8(sk)))
         return dict(eta=eta, nli_psd=psd, nli_power=pw, quadrant=q.reshape(n, 4), skipped=sk)
+
+    def cfm_all_channels_nli(self, case: Case, prep=None):
+        """or_cfm_all_channels_nli: the closed-form model (gn_closed_form.hpp:70-144)."""
+        prep = prep or self.prepare(case)
+        g = prep["grid"]
+        n = g.n
+        spans, keep = self._spans(prep["spans"])
+        gam = np.ascontiguousarray(prep["gamma"], dtype=np.float64)
+        b = np.ascontiguousarray(prep["betas"], dtype=np.float64)
+        eta, psd, pw = np.zeros(n), np.zeros(n), np.zeros(n)
+        sk = np.zeros(n, np.uint8)
+        self._chk(self.lib.or_cfm_all_channels_nli(C.byref(g), spans, len(prep["spans"]), _dp(b),
+                                                   _dp(gam), _dp(eta), _dp(psd), _dp(pw), _u8(sk)))
+        return dict(eta=eta, nli_psd=psd, nli_power=pw, skipped=sk)
 
     def nli_psd_at(self, case: Case, gamma, nu, prep=None):
         prep = prep or self.prepare(case)

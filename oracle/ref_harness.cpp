@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "support/test_helpers.hpp"
+#include "uwblink/gn_closed_form.hpp"
 #include "uwblink/gn_integral.hpp"
 #include "uwblink/link_optimizer.hpp"
 
@@ -223,6 +224,28 @@ int ref_all_channels_nli(const RefCase* c, double* eta, double* nli_psd, double*
     if (quad4) std::memcpy(quad4, r.quadrant.data(), n * 4 * sizeof(double));
     if (skipped) std::memcpy(skipped, r.skipped.data(), n);
     if (nli_seconds) *nli_seconds = r.elapsed_seconds;
+  });
+}
+
+// Closed-form model: power evolution + cfm_all_channels_nli (gn_closed_form.hpp:70).
+int ref_cfm_all_channels_nli(const RefCase* c, double* eta, double* nli_psd, double* nli_power,
+                             uint8_t* skipped, double* seconds) {
+  return guarded([&] {
+    const FibreSpec f = make_fibre(*c);
+    const ChannelGrid g = make_grid(*c);
+    const DistanceGrid zg = build_distance_grid(f.length_m, c->density);
+    RamanSolveOptions opt;
+    opt.include_raman = c->raman != 0;
+    const PowerEvolution evo = solve_power_evolution(f, g, zg, opt);
+    const std::vector<PowerEvolution> spans(static_cast<std::size_t>(f.span_count), evo);
+    const auto t0 = std::chrono::steady_clock::now();
+    const NliResult r = cfm_all_channels_nli(g, spans, make_betas(*c, f, g), f);
+    if (seconds) *seconds = secs(t0);
+    const std::size_t n = g.size();
+    if (eta) std::memcpy(eta, r.eta.data(), n * sizeof(double));
+    if (nli_psd) std::memcpy(nli_psd, r.nli_psd.data(), n * sizeof(double));
+    if (nli_power) std::memcpy(nli_power, r.nli_power.data(), n * sizeof(double));
+    if (skipped) std::memcpy(skipped, r.skipped.data(), n);
   });
 }
 

@@ -822,3 +822,98 @@ int or_assemble_link_report(const OrGrid* g, int span_count, const double* eta,
   totals3[2] = total_w > 0.0 ? 10.0 * log10(total_w / 1e-3) : -300.0;
   return OR_OK;
 }
+
+/* ---- closed-form model (gn_closed_form.hpp) ---------------------------- */
+
+/* phi_xpm gn_closed_form.hpp:23-27 */
+double or_phi_xpm(double f_i, double f_k, const double b[3]) {
+  const double bracket = b[0] + kPi * b[1] * (f_i + f_k) +
+                         (2.0 * kPi * kPi / 3.0) * b[2] * (f_i * f_i + f_i * f_k + f_k * f_k);
+  return -4.0 * kPi * kPi * bracket * (f_k - f_i);
+}
+
+/* phi_spm :30-33 */
+double or_phi_spm(double f_i, const double b[3]) {
+  return -4.0 * kPi * kPi *
+         (b[0] + 2.0 * kPi * b[1] * f_i + 2.0 * kPi * kPi * b[2] * f_i * f_i);
+}
+
+/* effective_alpha :37-47 (bisection, 200 iterations) */
+double or_effective_alpha(double l_eff, double length) {
+  if (l_eff >= length) return 1e-12;
+  double lo = 1e-12, hi = 1.0;
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    const double val = (1.0 - exp(-mid * length)) / mid;
+    if (val > l_eff) lo = mid; else hi = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+/* detail::xpm_island :53-59 */
+double or_xpm_island(double phi_abs, double bch, double alpha) {
+  const double x = phi_abs * bch / (2.0 * alpha);
+  if (x < 1e-3) return (0.75 - (5.0 / 24.0) * x * x) * bch * bch / (alpha * alpha);
+  return 2.0 * bch / (alpha * phi_abs) * atan(x) - log1p(x * x) / (phi_abs * phi_abs);
+}
+
+/* cfm_all_channels_nli :70-144 (kCfmSpmCalibration / kCfmXpmCalibration :67-68) */
+int or_cfm_all_channels_nli(const OrGrid* g, const OrSpan* spans, int n_spans, const double b[3],
+                            const double* gamma_ch, double* eta, double* nli_psd,
+                            double* nli_power, uint8_t* skipped) {
+  const int n = g->n;
+  const double spm_cal = 1.9641, xpm_cal = 1.0571;
+  for (int i = 0; i < n; ++i) {
+    eta[i] = nli_psd[i] = nli_power[i] = 0.0;
+    skipped[i] = 0;
+  }
+  if (n_spans < 1) return fail(OR_CONFIG_ERROR, "cfm: need at least one span");
+  double* alpha_eff = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  for (int s = 0; s < n_spans; ++s) {
+    const OrSpan* ev = &spans[s];
+    const double span_len = ev->length;
+    for (int i = 0; i < n; ++i) {
+      alpha_eff[i] = 1e-12;
+      double l_eff = 0.0;
+      for (int m = 0; m < ev->steps; ++m)
+        l_eff += exp(ev->log_rho[(size_t)i * ev->steps + m]) * ev->width[m];
+      if (l_eff > 0.0) alpha_eff[i] = or_effective_alpha(l_eff < span_len ? l_eff : span_len, span_len);
+    }
+    for (int i = 0; i < n; ++i) {
+      if (g->guard[i] || g->psd[i] <= 0.0) {
+        skipped[i] = 1;
+        continue;
+      }
+      const double p_i = g->psd[i] * g->bch;
+      const double f_i = g->freq[i] - g->centre;
+      double eta_i = 0.0;
+      const double phi_i = fabs(or_phi_spm(f_i, b));
+      const double a_i = alpha_eff[i];
+      const double spm_arg = phi_i * g->bch * g->bch / (8.0 * a_i);
+      double spm;
+      if (spm_arg < 1e-3)
+        spm = (kPi / (a_i * (phi_i > 1e-300 ? phi_i : 1e-300))) * spm_arg;
+      else
+        spm = (kPi / (a_i * phi_i)) * asinh(spm_arg);
+      eta_i += spm_cal * (16.0 / 27.0) * (gamma_ch[i] * gamma_ch[i] / (g->bch * g->bch)) * spm;
+      for (int k = 0; k < n; ++k) {
+        if (k == i || g->guard[k] || g->psd[k] <= 0.0) continue;
+        const double p_k = g->psd[k] * g->bch;
+        const double phik = fabs(or_phi_xpm(f_i, g->freq[k] - g->centre, b));
+        const double island = or_xpm_island(phik, g->bch, alpha_eff[k]);
+        const double ratio = p_k / p_i;
+        eta_i += xpm_cal * (32.0 / 27.0) * (gamma_ch[i] * gamma_ch[k] / (g->bch * g->bch)) *
+                 ratio * ratio * island;
+      }
+      eta[i] += eta_i;
+    }
+  }
+  free(alpha_eff);
+  for (int i = 0; i < n; ++i) {
+    if (skipped[i]) continue;
+    const double p = g->psd[i] * g->bch;
+    nli_power[i] = eta[i] * p * p * p;
+    nli_psd[i] = nli_power[i] / g->bch;
+  }
+  return OR_OK;
+}

@@ -101,6 +101,8 @@ SIGNATURES = {
                                        DP, C.POINTER(NliCfg), C.POINTER(NliResultC)]),
     "uwb_nli_psd_at": (C.c_int, [C.c_void_p, C.POINTER(Grid), C.c_int, C.POINTER(Span), DP,
                                  C.POINTER(NliCfg), C.c_int, DP, DP, DP, DP]),
+    "uwb_cfm_all_channels_nli": (C.c_int, [C.c_void_p, C.POINTER(Grid), C.c_int, C.POINTER(Span),
+                                           DP, DP, C.POINTER(NliResultC)]),
     "uwb_channel_nli": (C.c_int, [C.c_void_p, C.POINTER(Grid), C.c_int, C.POINTER(Span), DP,
                                   C.c_double, C.POINTER(NliCfg), C.c_int, DP, DP]),
     "uwb_power_evolution": (C.c_int, [C.c_void_p, C.POINTER(Grid), C.POINTER(Fibre),

@@ -63,6 +63,8 @@ struct uwb_ctx {
   uwb::DBuf eta, nli_psd, nli_power, quad, skipped;
   // uwb_evaluate_link_many: the batch's launch profiles and reports
   uwb::DBuf batch_psd, batch_report, batch_ode;
+  // closed-form model (uwb_cfm.cu)
+  uwb::DBuf cfm_in, cfm_work, cfm_span;
   struct BatchState {  // overlapped uwb_evaluate_link_many (second ODE stream)
     cudaStream_t s_ode = nullptr;
     cudaEvent_t ev_start = nullptr, ev_ode[2] = {nullptr, nullptr}, ev_nli[2] = {nullptr, nullptr};

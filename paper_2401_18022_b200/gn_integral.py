@@ -455,6 +455,29 @@ def all_channels_nli(grid: ChannelGrid, spans, betas: BetaCoefficients, fibre, c
     return NliResult(eta, psd, pw, quad.reshape(n, 4), sk, res.elapsed_seconds)
 
 
+def cfm_all_channels_nli(grid: ChannelGrid, spans, betas: BetaCoefficients, fibre,
+                         engine=None, gamma=None) -> NliResult:
+    """Closed-form SPM + XPM model, gn_closed_form.hpp:70-144 (on the device).
+    `fibre` supplies gamma_at per channel (:84-87); `gamma` overrides it.
+    The quadrant array is zeros, like the reference's."""
+    eng = engine or get_engine()
+    n = grid.size()
+    if not spans:
+        raise ConfigError("cfm: need at least one span")
+    for s in spans:
+        if s.channels() != n:
+            raise ConfigError("cfm: span evolution does not match the grid")
+    gam = N.f64(gamma) if gamma is not None else fibre.sample(grid.freq, 1.5e-6)["gamma"]
+    eta, psd, pw, quad = np.zeros(n), np.zeros(n), np.zeros(n), np.zeros(4 * n)
+    sk = np.zeros(n, np.uint8)
+    res = N.NliResultC(N.dptr(eta), N.dptr(psd), N.dptr(pw), N.dptr(quad), N.u8ptr(sk), 0.0)
+    g, sp = grid._c(), _spans_c(spans)
+    b = betas.as_array()
+    N.check(eng.lib.uwb_cfm_all_channels_nli(eng.h, N.C.byref(g), len(spans), sp, N.dptr(b),
+                                             N.dptr(gam), N.C.byref(res)))
+    return NliResult(eta, psd, pw, quad.reshape(n, 4), sk, res.elapsed_seconds)
+
+
 # ----------------------------------------------------------------- full SNR evaluation
 @dataclass
 class LinkConfig:

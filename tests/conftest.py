@@ -21,6 +21,12 @@ def golden():
 
 
 @pytest.fixture(scope="session")
+def golden_cfm():
+    with open(os.path.join(ROOT, "tests", "golden", "golden_cfm.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.fixture(scope="session")
 def oracle():
     from pyoracle import Oracle, build_oracle
 

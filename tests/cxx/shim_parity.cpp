@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "support/test_helpers.hpp"
+#include "uwblink_b200/gn_closed_form.hpp"
 #include "uwblink_b200/gn_integral.hpp"
 
 using namespace uwblink;
@@ -85,7 +86,83 @@ struct Band11 {
 
 }  // namespace
 
+// test_closed_form.cpp:104-121
+struct CBandComb {
+  FibreSpec fibre = default_fibre();
+  ChannelGrid grid;
+  BetaCoefficients betas;
+  std::vector<PowerEvolution> spans;
+  explicit CBandComb(std::size_t n_channels, double centre_lambda = 1550e-9,
+                     double power_dbm = 0.0, bool raman = false) {
+    grid = make_uniform_grid(n_channels, 100e9, 96e9, lambda_to_freq(centre_lambda));
+    set_uniform_launch(grid, dbm_to_watt(power_dbm));
+    betas = beta_from_dispersion(fibre.dispersion, centre_lambda);
+    RamanSolveOptions opt;
+    opt.include_raman = raman;
+    spans.push_back(
+        solve_power_evolution(fibre, grid, build_distance_grid(fibre.length_m, 1.4), opt));
+  }
+};
+
+void closed_form_checks() {
+  run("cfm_tracks_integral_away_from_zdw", [] {  // test_closed_form.cpp:125-136
+    CBandComb comb(9);
+    GnSolverConfig gn;
+    gn.n_r = 200;
+    const NliResult full = b2::all_channels_nli(comb.grid, comb.spans, comb.betas, comb.fibre, gn);
+    const NliResult cfm = b2::cfm_all_channels_nli(comb.grid, comb.spans, comb.betas, comb.fibre);
+    const NliResult ref = cfm_all_channels_nli(comb.grid, comb.spans, comb.betas, comb.fibre);
+    bool ok = true;
+    for (std::size_t ch = 0; ch < comb.grid.size(); ++ch)
+      ok = ok && cfm.eta[ch] > 0.0 && std::abs(uwtest::to_db(cfm.eta[ch] / full.eta[ch])) < 1.0;
+    const double rel = max_rel(cfm.eta, ref.eta);
+    return verdict(ok && rel < 1e-9, "rel vs reference %.3e", rel);
+  });
+  run("cfm_edge_handling", [] {  // :158-180
+    CBandComb comb(5);
+    ChannelGrid gg = comb.grid;
+    gg.guard[2] = 1;
+    gg.psd[2] = 0.0;
+    const NliResult r = b2::cfm_all_channels_nli(gg, comb.spans, comb.betas, comb.fibre);
+    bool ok = r.skipped[2] == 1 && r.eta[2] == 0.0 && r.eta[1] > 0.0;
+    int thrown = 0;
+    try {
+      (void)b2::cfm_all_channels_nli(comb.grid, {}, comb.betas, comb.fibre);
+    } catch (const ConfigError&) {
+      ++thrown;
+    }
+    CBandComb other(7);
+    try {
+      (void)b2::cfm_all_channels_nli(comb.grid, other.spans, comb.betas, comb.fibre);
+    } catch (const ConfigError&) {
+      ++thrown;
+    }
+    ok = ok && thrown == 2;
+    return verdict(ok, "%g", ok ? 1.0 : 0.0);
+  });
+  run("cfm_undershoots_near_zdw", [] {  // :182-207
+    CBandComb comb(5, 1302.3e-9, 2.0, true);
+    GnSolverConfig gn;
+    gn.n_r = 150;
+    const NliResult full = b2::all_channels_nli(comb.grid, comb.spans, comb.betas, comb.fibre, gn);
+    const NliResult cfm = b2::cfm_all_channels_nli(comb.grid, comb.spans, comb.betas, comb.fibre);
+    const NliResult ref = cfm_all_channels_nli(comb.grid, comb.spans, comb.betas, comb.fibre);
+    std::size_t worst = 0;
+    double gap_w = 0.0;
+    for (std::size_t ch = 0; ch < comb.grid.size(); ++ch) {
+      const double gap = std::abs(uwtest::to_db(cfm.eta[ch] / full.eta[ch]));
+      if (gap > gap_w) {
+        gap_w = gap;
+        worst = ch;
+      }
+    }
+    const double rel = max_rel(cfm.eta, ref.eta);
+    return verdict(cfm.eta[worst] < full.eta[worst] && rel < 1e-9, "rel vs reference %.3e", rel);
+  });
+}
+
 int main() {
+  closed_form_checks();
   // --- hyperbolic vs Cartesian, test_gn_integral.cpp:226-235 (+ B200 == CPU)
   run("toy3_nli_psd_at_vs_reference_and_cartesian", [] {
     ToyCase toy;

@@ -347,3 +347,30 @@ def test_mixed_precision_evaluate_link(golden, mixed_engine):
 def test_precision_mode_errors(engine):
     with pytest.raises(uwb.ConfigError):
         engine.set_precision("fp16")
+
+
+# ---------------------------------------------------------------- closed-form model (§8 f4)
+@pytest.mark.parametrize("name", ["cband11", "oband11", "toy5_guard", "toy3_3span", "uwb589_0.95",
+                                  "uwb589_random_launch"])
+def test_cfm_all_channels_nli_matches_reference(name, golden_cfm, oracle, engine):
+    """cfm_all_channels_nli (gn_closed_form.hpp:70-144) on the device vs the
+    reference's own outputs, on the oracle's (bit-exact) ODE tables."""
+    rec = golden_cfm["cfm_all_channels_nli"][name]
+    case = Case.from_json(rec["case"])
+    prep = oracle.prepare(case)
+    grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
+    r = uwb.cfm_all_channels_nli(grid, spans, betas, None, engine=engine, gamma=gamma)
+    assert np.array_equal(r.skipped, np.array(rec["skipped"], np.uint8))
+    assert _rel(r.eta, rec["eta"]) < NLI_TOL
+    assert _rel(r.nli_psd, rec["nli_psd"]) < NLI_TOL
+    assert _rel(r.nli_power, rec["nli_power"]) < NLI_TOL
+    assert np.all(np.asarray(r.quadrant) == 0.0)
+    assert r.elapsed_seconds > 0.0
+
+
+def test_cfm_config_errors(oracle, engine):
+    case = oband11()
+    prep = oracle.prepare(case)
+    grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
+    with pytest.raises(uwb.ConfigError):
+        uwb.cfm_all_channels_nli(grid, [], betas, None, engine=engine, gamma=gamma)
