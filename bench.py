@@ -317,6 +317,42 @@ def run_engine(args):
                 torch.cuda.synchronize(dev)
                 vs.append(e0.elapsed_time(e1))
             variants[f"n_r{nr}_density{dens}"] = {"s_per_eval": float(np.median(vs)) / 1e3}
+        # compensated-FP32 integrand (config 4 column): same workload, time and
+        # max relative eta deviation from the FP64 evaluation
+        # (one prepared link per context: prepare the FP64 reference again)
+        r64 = uwb.ResidentLink(fibre, grid, lc, engine=eng)
+        r64.run(psd.data_ptr(), report.data_ptr(), sp)
+        torch.cuda.synchronize(dev)
+        eta64 = report[:n].cpu().numpy().copy()
+        eng.set_precision("mixed")
+        rm = uwb.ResidentLink(fibre, grid, lc, engine=eng)
+        eng.set_precision("fp64")
+        rm.run(psd.data_ptr(), report.data_ptr(), sp)
+        vs = []
+        for _ in range(5):
+            flush.zero_()
+            e0.record(stream)
+            rm.run(psd.data_ptr(), report.data_ptr(), sp)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            vs.append(e0.elapsed_time(e1))
+        etam = report[:n].cpu().numpy()
+        act = eta64 > 0
+        variants["mixed_precision"] = {
+            "s_per_eval": float(np.median(vs)) / 1e3,
+            "max_rel_eta_vs_fp64": float(np.max(np.abs(etam[act] - eta64[act]) / eta64[act])),
+            "note": "compensated FP32 integrand (uwb_set_precision MIXED); not the headline"}
+        # closed-form model on the same ODE tables: device time
+        try:
+            zg = uwb.build_distance_grid(fibre.length_m, lc.gn.mean_step_density)
+            evo = uwb.solve_power_evolution(fibre, grid, zg, uwb.RamanSolveOptions(True), engine=eng)
+            betas = uwb.beta_from_dispersion(fibre, 299792458.0 / grid.centre)
+            cf = [uwb.cfm_all_channels_nli(grid, [evo], betas, fibre, engine=eng).elapsed_seconds
+                  for _ in range(5)]
+            variants["closed_form_cfm"] = {"s_per_nli": float(np.median(cf)),
+                                           "api": "uwb_cfm_all_channels_nli (device time)"}
+        except Exception as exc:  # report, never hide
+            variants["closed_form_cfm"] = {"error": str(exc)}
         # optimiser-style batch (config 5): 56 independent launch profiles through
         # uwb_evaluate_link_many, the ODE of e+1 overlapped with the integrand of e
         # (host psd in, losses/reports out; wall clock around the whole batch)

@@ -4,6 +4,9 @@ For N_R x N_M-density settings: device time of one full SNR evaluation
 (ResidentLink, median of 3, CUDA events) and the NLI accuracy against the
 (N_R=500, density 2.0) evaluation of the same engine (max / mean |d eta| in dB
 over active channels) -- the accuracy-vs-time trade-off of PAPER.md:126.
+Each setting also runs the compensated-FP32 integrand ("mixed",
+uwb_set_precision): its time and its max relative eta deviation from the FP64
+evaluation at the same setting (the "FP64 vs compensated FP32" column).
 
     python tools/sweep.py [--out profiles/r01_config4_sweep.json]
 """
@@ -33,7 +36,8 @@ psd = torch.tensor(grid.psd, dtype=torch.float64, device="cuda:0")
 n = grid.size()
 
 
-def run(nr, dens):
+def run(nr, dens, precision="fp64"):
+    eng.set_precision(precision)
     res = uwb.ResidentLink(fibre, grid, uwb.LinkConfig(gn=uwb.GnSolverConfig(n_r=nr, mean_step_density=dens)),
                            engine=eng)
     rep = torch.zeros(res.report_len, dtype=torch.float64, device="cuda:0")
@@ -57,9 +61,14 @@ for nr in [int(x) for x in a.n_r.split(",")]:
     for dens in [float(x) for x in a.density.split(",")]:
         t, eta, s = run(nr, dens)
         d = np.abs(10 * np.log10(eta[act] / eta_ref[act]))
+        tm, eta_m, sm = run(nr, dens, "mixed")
+        rel_m = np.abs(eta_m[act] - eta[act]) / eta[act]
         rows.append({"n_r": nr, "density": dens, "eval_ms": t, "nli_kernel_ms": s["kernel_ms"],
                      "evaluated_points": s["evaluated_points"], "active_points": s["active_points"],
-                     "max_abs_deta_db": float(d.max()), "mean_abs_deta_db": float(d.mean())})
+                     "max_abs_deta_db": float(d.max()), "mean_abs_deta_db": float(d.mean()),
+                     "mixed_eval_ms": tm, "mixed_nli_kernel_ms": sm["kernel_ms"],
+                     "mixed_max_rel_eta_vs_fp64": float(rel_m.max()),
+                     "mixed_max_abs_deta_db_vs_fp64": float(np.max(np.abs(10 * np.log10(eta_m[act] / eta[act]))))})
         print(json.dumps(rows[-1]), flush=True)
 out = {"reference_setting": {"n_r": 500, "density": 2.0, "eval_ms": t_ref}, "rows": rows,
        "workload": "589ch O-U, 80 km, 0 dBm/ch, ISRS on; accuracy vs this engine at (500, 2.0)"}
