@@ -377,3 +377,41 @@ def test_cfm_config_errors(oracle, engine):
     grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
     with pytest.raises(uwb.ConfigError):
         uwb.cfm_all_channels_nli(grid, [], betas, None, engine=engine, gamma=gamma)
+
+
+# ---------------------------------------------------------------- acceptance checks on the device
+C0 = 299792458.0
+
+
+def _device_nli(engine, n_ch, lam, dbm, n_r, density, raman=True):
+    fibre = uwb.default_fibre()
+    grid = uwb.make_uniform_grid(n_ch, 100e9, 96e9, C0 / lam)
+    uwb.set_uniform_launch(grid, 1e-3 * 10 ** (dbm / 10))
+    zg = uwb.build_distance_grid(fibre.length_m, density)
+    evo = uwb.solve_power_evolution(fibre, grid, zg, uwb.RamanSolveOptions(raman), engine=engine)
+    betas = uwb.beta_from_dispersion(fibre, C0 / grid.centre)
+    cfg = uwb.GnSolverConfig(n_r=n_r, mean_step_density=density)
+    return uwb.all_channels_nli(grid, [evo], betas, fibre, cfg, engine=engine)
+
+
+def test_acceptance_c2_resolution_tradeoff(engine):
+    """acceptance_main.cpp:88-137 (C2) on the device: 64-ch C-band, (75, 0.95)
+    within 0.6 dB and (150, 1.4) within 0.15 dB of (500, 2.0).  The C2 worker
+    check (1 vs 4 identical) is test_deterministic_and_partition_independent;
+    its CPU-thread timing ratios have no device counterpart."""
+    ref = _device_nli(engine, 64, 1550e-9, 0.0, 500, 2.0)
+    coarse = _device_nli(engine, 64, 1550e-9, 0.0, 75, 0.95)
+    mid = _device_nli(engine, 64, 1550e-9, 0.0, 150, 1.4)
+    dev_c = np.max(np.abs(to_db(coarse.eta / ref.eta)))
+    dev_m = np.max(np.abs(to_db(mid.eta / ref.eta)))
+    assert dev_c <= 0.6 and dev_m <= 0.15, (dev_c, dev_m)
+
+
+def test_acceptance_c4_cubic_scaling_raman_off(engine):
+    """acceptance_main.cpp:183-217 (C4): +3 dB launch -> +9 dB NLI power within
+    0.01 dB and eta drift <= 1e-6 (16-ch C-band, Raman off, N_R 64, 0.8/km)."""
+    base = _device_nli(engine, 16, 1550e-9, 0.0, 64, 0.8, raman=False)
+    boost = _device_nli(engine, 16, 1550e-9, 3.0, 64, 0.8, raman=False)
+    gain = 10 * np.log10(boost.nli_power / base.nli_power)
+    assert np.max(np.abs(gain - 9.0)) <= 0.01
+    assert np.max(np.abs(boost.eta / base.eta - 1.0)) <= 1e-6
