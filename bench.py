@@ -342,6 +342,26 @@ def run_engine(args):
             "s_per_eval": float(np.median(vs)) / 1e3,
             "max_rel_eta_vs_fp64": float(np.max(np.abs(etam[act] - eta64[act]) / eta64[act])),
             "note": "compensated FP32 integrand (uwb_set_precision MIXED); not the headline"}
+        # continuous ODE stepping (uwb_set_ode_stepping): the reference's
+        # controller without the per-midpoint restart; eta within ~1e-10
+        eng.set_ode_stepping("continuous")
+        rc_ = uwb.ResidentLink(fibre, grid, lc, engine=eng)
+        eng.set_ode_stepping("restart")
+        rc_.run(psd.data_ptr(), report.data_ptr(), sp)
+        vs = []
+        for _ in range(5):
+            flush.zero_()
+            e0.record(stream)
+            rc_.run(psd.data_ptr(), report.data_ptr(), sp)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            vs.append(e0.elapsed_time(e1))
+        etac = report[:n].cpu().numpy()
+        variants["ode_continuous_stepping"] = {
+            "s_per_eval": float(np.median(vs)) / 1e3,
+            "ode_rhs": eng.last_ode_stats()["rhs_evals"],
+            "max_rel_eta_vs_restart": float(np.max(np.abs(etac[act] - eta64[act]) / eta64[act])),
+            "note": "uwb_set_ode_stepping CONTINUOUS (extension; not the headline)"}
         # closed-form model on the same ODE tables: device time
         try:
             zg = uwb.build_distance_grid(fibre.length_m, lc.gn.mean_step_density)

@@ -242,6 +242,17 @@ int uwb_fp64_peak(uwb_ctx* ctx, double* tflops);
 #define UWB_PRECISION_FP64 0
 #define UWB_PRECISION_MIXED 1
 int uwb_set_precision(uwb_ctx* ctx, int mode);
+/* Step-size policy of the device Raman ODE for subsequent calls/prepares.
+ * UWB_ODE_RESTART (default): the reference's -- Rk45::integrate restarts at
+ * every distance-grid midpoint with h0 = (z1 - z0)/100 (raman_power.hpp:107-
+ * 118, rk45.hpp:33).  UWB_ODE_CONTINUOUS: the same Dormand-Prince controller and
+ * tolerances, landing exactly on every midpoint, but the step size carries
+ * across midpoints instead of restarting (about 3x fewer RHS evaluations).
+ * An extension: results differ from the reference by the ODE's own truncation
+ * error. */
+#define UWB_ODE_RESTART 0
+#define UWB_ODE_CONTINUOUS 1
+int uwb_set_ode_stepping(uwb_ctx* ctx, int mode);
 /* Kernel launches issued by the last call (evidence for bench gpu_launches). */
 int uwb_last_launch_count(uwb_ctx* ctx);
 /* Device time (ms) of the last NLI integrand kernel and its inner-step count

@@ -123,6 +123,7 @@ SIGNATURES = {
                                           C.POINTER(C.c_ulonglong)]),
     "uwb_fp64_peak": (C.c_int, [C.c_void_p, DP]),
     "uwb_set_precision": (C.c_int, [C.c_void_p, C.c_int]),
+    "uwb_set_ode_stepping": (C.c_int, [C.c_void_p, C.c_int]),
     "uwb_last_launch_count": (C.c_int, [C.c_void_p]),
     "uwb_last_nli_stats": (C.c_int, [C.c_void_p, DP, DP, DP]),
     "uwb_last_nli_active": (C.c_int, [C.c_void_p, DP]),

@@ -46,6 +46,9 @@ namespace {
 #ifndef UWB_NLI_MIN_BLOCKS
 #define UWB_NLI_MIN_BLOCKS 2
 #endif
+#ifndef UWB_NLI_MIXED_MIN_BLOCKS
+#define UWB_NLI_MIXED_MIN_BLOCKS 3  // 80 registers: 6 warps per SMSP (10.9 -> 10.0 ms)
+#endif
 constexpr int kWarps = UWB_NLI_WARPS;  // warps per CTA
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -503,7 +506,8 @@ __device__ __forceinline__ double point_kernel_mixed(const NliParams& P, const W
 }
 
 template <int K, bool FULL, bool HOIST, bool MIXED>
-__global__ void __launch_bounds__(kWarps * 32, UWB_NLI_MIN_BLOCKS) nli_rows_kernel(const NliParams P) {
+__global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS : UWB_NLI_MIN_BLOCKS)
+    nli_rows_kernel(const NliParams P) {
   __shared__ WarpSmem s_w[kWarps];
   extern __shared__ double row_vals[];  // [kWarps][n_r]
   if (threadIdx.x < 16) {

@@ -30,6 +30,7 @@ struct OdeParams {
   const double* mid;     // [steps]
   double length;
   double rtol, atol;
+  int continuous;        // 0: restart at every midpoint like the reference; 1: carry h across
   double* log2rho;       // [n * col_stride] out: log2(rho) in the NLI layout
   double* log_rho;       // [n * col_stride] out: ln(rho) (may be null)
   double* rho_end;       // [n] out

@@ -508,6 +508,14 @@ int uwb_set_precision(uwb_ctx* c, int mode) {
   return UWB_OK;
 }
 
+int uwb_set_ode_stepping(uwb_ctx* c, int mode) {
+  if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  if (mode != UWB_ODE_RESTART && mode != UWB_ODE_CONTINUOUS)
+    return set_err(UWB_CONFIG_ERROR, "uwb_set_ode_stepping: unknown mode");
+  c->ode_continuous = mode == UWB_ODE_CONTINUOUS ? 1 : 0;
+  return UWB_OK;
+}
+
 int uwb_fp64_peak(uwb_ctx* c, double* tflops) {
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
   cudaSetDevice(c->device);

@@ -50,6 +50,7 @@ struct uwb_ctx {
   int device = 0;
   int sm_count = 0;
   int precision = 0;  // UWB_PRECISION_FP64 / _MIXED (uwb_set_precision)
+  int ode_continuous = 0;  // UWB_ODE_RESTART / _CONTINUOUS (uwb_set_ode_stepping)
   int cc_major = 0, cc_minor = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;

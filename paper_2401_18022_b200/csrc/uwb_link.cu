@@ -356,6 +356,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   O.length = fb->length_m;
   O.rtol = pr->rtol;
   O.atol = pr->atol;
+  O.continuous = c->ode_continuous;
   O.log2rho = const_cast<double*>(P.log2rho);
   O.log_rho = nullptr;
   O.rho_end = d_rho_end;
@@ -724,6 +725,7 @@ int uwb_power_evolution(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre
   O.length = fibre->length_m;
   O.rtol = link->rtol > 0 ? link->rtol : 1e-9;
   O.atol = link->atol > 0 ? link->atol : 1e-16;
+  O.continuous = c->ode_continuous;
   O.log2rho = d_l2;
   O.log_rho = d_ln;
   O.rho_end = d_re;

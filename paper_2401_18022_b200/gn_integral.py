@@ -299,6 +299,16 @@ class Engine:
         N.check(self.lib.uwb_set_precision(self.h, modes[mode]))
         self.precision = mode
 
+    def set_ode_stepping(self, mode: str):
+        """Raman ODE step-size policy for subsequent calls: "restart" (default,
+        the reference's restart at every midpoint) or "continuous" (the step
+        size carries across midpoints; include/uwb_nli.h)."""
+        modes = {"restart": 0, "continuous": 1}
+        if mode not in modes:
+            raise ConfigError(f"set_ode_stepping: unknown mode {mode!r}")
+        N.check(self.lib.uwb_set_ode_stepping(self.h, modes[mode]))
+        self.ode_stepping = mode
+
     def fp64_peak_tflops(self):
         t = N.C.c_double()
         N.check(self.lib.uwb_fp64_peak(self.h, N.C.byref(t)))

@@ -415,3 +415,46 @@ def test_acceptance_c4_cubic_scaling_raman_off(engine):
     gain = 10 * np.log10(boost.nli_power / base.nli_power)
     assert np.max(np.abs(gain - 9.0)) <= 0.01
     assert np.max(np.abs(boost.eta / base.eta - 1.0)) <= 1e-6
+
+
+# ---------------------------------------------------------------- ODE step-size policy extension
+@pytest.fixture
+def continuous_engine(engine):
+    engine.set_ode_stepping("continuous")
+    yield engine
+    engine.set_ode_stepping("restart")
+
+
+@pytest.mark.parametrize("name", ["uwb589_75_0.95", "uwb589_random_launch"])
+def test_continuous_ode_stepping_within_tolerance(name, golden, continuous_engine):
+    """uwb_set_ode_stepping(CONTINUOUS): the reference's Dormand-Prince
+    controller without the restart at every midpoint (~3x fewer RHS).  Full
+    evaluation within the north-star tolerance of the reference (observed
+    2.5e-10 eta, 5e-9 dB)."""
+    rec = golden["evaluate_link"][name]
+    case = Case.from_json(rec["case"])
+    grid, fibre = product_scenario(case)
+    lc = uwb.LinkConfig(gn=cfg_of(case), raman=uwb.RamanSolveOptions(bool(case.raman)))
+    rep = uwb.evaluate_link(fibre, grid, lc, engine=continuous_engine)
+    eta_ref = np.array(rec["eta"])
+    act = eta_ref > 0
+    assert _rel(rep.eta[act], eta_ref[act]) < 1e-8
+    assert np.max(np.abs(rep.snr_db[act] - np.array(rec["snr_db"])[act])) < 1e-6
+
+
+@pytest.mark.parametrize("name", ["uwb589", "cband11", "toy3"])
+def test_continuous_ode_power_evolution(name, golden, continuous_engine):
+    rec = golden["power_evolution"][name]
+    case = Case.from_json(rec["case"])
+    grid, fibre = product_scenario(case)
+    zg = uwb.build_distance_grid(case.length_m, case.density)
+    evo = uwb.solve_power_evolution(fibre, grid, zg, uwb.RamanSolveOptions(bool(case.raman)),
+                                    engine=continuous_engine)
+    np.testing.assert_allclose(evo.rho_end, rec["rho_end"], rtol=1e-8)
+    for i, v in rec["log_rho_samples"]:
+        assert abs(evo.log_rho[i] - v) < 1e-8
+
+
+def test_ode_stepping_mode_errors(engine):
+    with pytest.raises(uwb.ConfigError):
+        engine.set_ode_stepping("adaptive")

@@ -21,8 +21,10 @@ p.add_argument("--density", type=float, default=1.4)
 p.add_argument("--reps", type=int, default=7)
 p.add_argument("--tag", default=os.environ.get("UWB_LIB_PATH", "main"))
 p.add_argument("--grid", default="uwb589", choices=["uwb589", "oband11", "cband11"])
+p.add_argument("--precision", default="fp64", choices=["fp64", "mixed"])
 a = p.parse_args()
 eng = uwb.Engine(0)
+eng.set_precision(a.precision)
 if a.grid == "uwb589":
     grid = uwb.make_default_uwb_grid()
     uwb.set_uniform_launch(grid, 1e-3)
