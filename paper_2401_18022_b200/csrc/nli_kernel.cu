@@ -154,8 +154,11 @@ __constant__ double c_s16[4] = {kS16c1, kS16c2, kS16c3, kS16c4};
 __constant__ double c_c16[5] = {kC16c0, kC16c1, kC16c2, kC16c3, kC16c4};
 __constant__ double c_tab_cos16[16] = UWB_COS_TABLE16;
 __constant__ double c_tab_sin16[16] = UWB_SIN_TABLE16;
-__shared__ double s_cos16[16];
-__shared__ double s_sin16[16];
+// (cos, sin)(k pi/8) interleaved: one 128-bit LDS per lookup (the 256-byte
+// table costs at most a 2-way conflict, q vs q + 8, i.e. the same wavefronts
+// as two 64-bit lookups in two 128-byte tables, with one instruction fewer
+// and no second base address)
+__shared__ double2 s_cs16[16];
 
 __device__ __forceinline__ void dev_sincos_table(double x, double* c_out, double* s_out) {
   const double t = fma(x, c_red8[0], kMagic);
@@ -173,7 +176,8 @@ __device__ __forceinline__ void dev_sincos_table(double x, double* c_out, double
   pc = fma(pc, z, c_c16[1]);
   pc = fma(pc, z, c_c16[0]);
   const double cr = fma(pc, z, 1.0);
-  const double tc = s_cos16[q], ts = s_sin16[q];
+  const double2 cs = s_cs16[q];
+  const double tc = cs.x, ts = cs.y;
   *c_out = fma(tc, cr, -(ts * sr));
   *s_out = fma(ts, cr, tc * sr);
 }
@@ -512,8 +516,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
   extern __shared__ double row_vals[];  // [kWarps][n_r]
   if (threadIdx.x < 16) {
     s_exp2_tab[threadIdx.x] = c_exp2_tab16[threadIdx.x];
-    s_cos16[threadIdx.x] = c_tab_cos16[threadIdx.x];
-    s_sin16[threadIdx.x] = c_tab_sin16[threadIdx.x];
+    s_cs16[threadIdx.x] = make_double2(c_tab_cos16[threadIdx.x], c_tab_sin16[threadIdx.x]);
     if (MIXED) {
       s_exp2_tabf[threadIdx.x] = __double2float_rn(c_exp2_tab16[threadIdx.x]);
       s_cos16f[threadIdx.x] = __double2float_rn(c_tab_cos16[threadIdx.x]);
