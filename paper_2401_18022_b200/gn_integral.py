@@ -208,6 +208,10 @@ class FibreSpec:
     length_m: float = 80e3
     span_count: int = 1
     flat_alpha_db_km: float | None = None  # None = default wavelength-dependent loss
+    # RamanGainCurve override (fibre_model.hpp:213-219): gain table x [Hz],
+    # y [1/(W m)]; None = the built-in triangle (:344-347)
+    raman_x: object = None
+    raman_y: object = None
 
     def sample(self, freq, lambda_beta):
         lib = N.load()
@@ -220,8 +224,13 @@ class FibreSpec:
         N.check(lib.uwb_model_fibre(kind, float(self.flat_alpha_db_km or 0.0), n, N.dptr(freq),
                                     float(lambda_beta), N.C.byref(s)))
         rn = s.raman_n
+        rx, ry = np.array(s.raman_x[:rn]), np.array(s.raman_y[:rn])
+        if self.raman_x is not None:
+            rx, ry = N.f64(self.raman_x), N.f64(self.raman_y)
+            if rx.size < 2 or rx.size != ry.size or np.any(np.diff(rx) <= 0):
+                raise ConfigError("raman gain: table must ascend and have >= 2 rows")
         return dict(alpha=alpha, aeff=aeff, gamma=gamma, beta=np.array(s.beta[:]),
-                    raman_x=np.array(s.raman_x[:rn]), raman_y=np.array(s.raman_y[:rn]),
+                    raman_x=rx, raman_y=ry,
                     raman_aeff_ref=s.raman_aeff_ref, dispersion=np.array(s.dispersion[:]))
 
 

@@ -458,3 +458,36 @@ def test_continuous_ode_power_evolution(name, golden, continuous_engine):
 def test_ode_stepping_mode_errors(engine):
     with pytest.raises(uwb.ConfigError):
         engine.set_ode_stepping("adaptive")
+
+
+def test_power_evolution_gain_table_with_gap(oracle, engine):
+    """A Raman gain table with a zero stretch between two gain lobes: the
+    device's contiguous window-edge pieces (raman_segments fills the gap with
+    a zero piece) against the C oracle's dense mat-vec on the same table."""
+    import ctypes as C
+    rx = np.array([0.0, 10e12, 20e12, 25e12, 100e12])
+    ry = np.array([0.2e-3, 0.0, 0.0, 0.2e-3, 0.0])
+    case = Case(uwb_default=1, n_r=8, density=0.95, raman=1, name="gap")
+    # oracle: default fibre with the table replaced
+    f, g = oracle.fibre(case), oracle.grid(case)
+    f.raman_gain.n = rx.size
+    for k in range(rx.size):
+        f.raman_gain.x[k], f.raman_gain.y[k] = rx[k], ry[k]
+    zg = oracle.distance_grid(case.length_m, case.density)
+    n, s = g.n, zg["steps"]
+    lr, re, ev = np.zeros(n * s), np.zeros(n), C.c_long()
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    rc = oracle.lib.or_power_evolution(C.byref(f), C.byref(g), dp(zg["mid"]), s,
+                                       C.c_double(case.length_m), 1, dp(lr), dp(re), C.byref(ev))
+    assert rc == 0
+    grid, fibre = product_scenario(case)
+    fibre.raman_x, fibre.raman_y = rx, ry
+    evo = uwb.solve_power_evolution(fibre, grid, uwb.build_distance_grid(case.length_m, case.density),
+                                    uwb.RamanSolveOptions(True), engine=engine)
+    np.testing.assert_allclose(evo.log_rho, lr, rtol=0, atol=1e-9)
+    np.testing.assert_allclose(evo.rho_end, re, rtol=1e-9)
+    # the table really couples channels: differs from the default triangle
+    base = uwb.solve_power_evolution(uwb.default_fibre(), grid,
+                                     uwb.build_distance_grid(case.length_m, case.density),
+                                     uwb.RamanSolveOptions(True), engine=engine)
+    assert np.max(np.abs(base.log_rho - evo.log_rho)) > 1e-3
