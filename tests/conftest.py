@@ -27,6 +27,12 @@ def golden_cfm():
 
 
 @pytest.fixture(scope="session")
+def golden_stress():
+    with open(os.path.join(ROOT, "tests", "golden", "golden_stress.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.fixture(scope="session")
 def oracle():
     from pyoracle import Oracle, build_oracle
 

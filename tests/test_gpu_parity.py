@@ -491,3 +491,17 @@ def test_power_evolution_gain_table_with_gap(oracle, engine):
                                      uwb.build_distance_grid(case.length_m, case.density),
                                      uwb.RamanSolveOptions(True), engine=engine)
     assert np.max(np.abs(base.log_rho - evo.log_rho)) > 1e-3
+
+
+@pytest.mark.parametrize("name", ["oband101", "oband101_simpson_nr80"])
+def test_stress_oband101_matches_reference(name, golden_stress, oracle, engine):
+    """BASELINE config 2 stress variant: 101 channels straddling the
+    zero-dispersion wavelength (MCI-dominated, 63 % sinc-branch points)."""
+    rec = golden_stress["all_channels_nli"][name]
+    case = Case.from_json(rec["case"])
+    prep = oracle.prepare(case)
+    grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
+    r = uwb.all_channels_nli(grid, spans, betas, None, cfg_of(case), engine=engine, gamma=gamma)
+    assert np.array_equal(r.skipped, np.array(rec["skipped"], np.uint8))
+    assert _rel(r.eta, rec["eta"]) < NLI_TOL
+    assert _rel(np.asarray(r.quadrant).ravel(), np.asarray(rec["quadrant"]).ravel()) < NLI_TOL
