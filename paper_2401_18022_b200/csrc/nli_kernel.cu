@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "nli_kernel.cuh"
 #include "uwb_devmath.cuh"
@@ -877,23 +878,29 @@ size_t row_smem(int n_r) { return static_cast<size_t>(kWarps) * n_r * sizeof(dou
 // static WarpSmem + dynamic row arrays may pass the 48 KB default: raise the
 // kernel's dynamic limit once per (kernel, size) high-water mark
 void allow_row_smem(RowKernel k, int n_r) {
-  static RowKernel seen_k[64];
-  static size_t seen_b[64];
+  // The attribute is per (device, kernel); contexts on several devices are
+  // driven from concurrent host threads (optimise_launch_powers), hence the lock.
+  struct Seen {
+    int dev;
+    RowKernel k;
+    size_t b;
+  };
+  static std::mutex mu;
+  static Seen seen[128];
   static int n_seen = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
   const size_t b = row_smem(n_r);
+  std::lock_guard<std::mutex> lock(mu);
   for (int i = 0; i < n_seen; ++i)
-    if (seen_k[i] == k) {
-      if (seen_b[i] >= b) return;
-      seen_b[i] = b;
+    if (seen[i].dev == dev && seen[i].k == k) {
+      if (seen[i].b >= b) return;
+      seen[i].b = b;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b));
       return;
     }
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b));
-  if (n_seen < 64) {
-    seen_k[n_seen] = k;
-    seen_b[n_seen] = b;
-    ++n_seen;
-  }
+  if (n_seen < 128) seen[n_seen++] = Seen{dev, k, b};
 }
 }  // namespace
 

@@ -78,63 +78,65 @@ __global__ void link_channels_kernel(LinkDev L) {
   L.tmp[2 * L.n + i] = l2;
 }
 
-// Ordered sums (loss, capacity, powers) in channel order (:224-235).  The
-// block stages the per-channel terms in shared memory, then one thread runs
-// the reference's sequential sums out of shared memory (the order is part of
-// the result; a global-memory loop costs a dependent L2 round trip per channel).
+// Link totals (loss, capacity, total and per-band power, :224-235).  One
+// warp per sum: lane l adds a contiguous run of channels in ascending order,
+// then a fixed xor-shuffle tree combines the 32 partials.  The order is fixed
+// (results are reproducible and identical on every path) but it is not the
+// reference's single sequential loop, so totals agree with the reference to
+// rounding (~1e-16 relative), not bit for bit.  Warp 0: loss, capacity, total
+// power; warp 1 + b: band b (bands beyond the warps loop).
 constexpr int kTotalsThreads = 256;
 constexpr int kMaxBands = 16;
 
+__device__ __forceinline__ double warp_sum_fixed(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __global__ void __launch_bounds__(kTotalsThreads) link_totals_kernel(LinkDev L) {
-  extern __shared__ double sm_tot[];
-  double* sp = sm_tot;           // [n] p (< 0: inactive)
-  double* sc = sp + L.n;         // [n] capacity
-  double* sl = sc + L.n;         // [n] log2(1 + snr)
-  int* sb = reinterpret_cast<int*>(sl + L.n);  // [n] band
-  for (int i = threadIdx.x; i < L.n; i += blockDim.x) {
-    sp[i] = L.tmp[i];
-    sc[i] = L.tmp[L.n + i];
-    sl[i] = L.tmp[2 * L.n + i];
-    sb[i] = L.band ? L.band[i] : -1;
-  }
-  __syncthreads();
-  // thread 0: loss, capacity, total power; thread 32 + b (another warp, so
-  // the loops run concurrently): band b.  Each sum runs over the channels in
-  // ascending order, like the reference's loop.
-  const int nb = L.n_bands < kMaxBands ? L.n_bands : kMaxBands;
-  double* op = L.out + 4 * L.n + 3;
-  double* oc = op + L.n_bands;
-  if (threadIdx.x >= 32 && threadIdx.x < 32 + nb) {
-    const int b = threadIdx.x - 32;
-    double bp = 0.0, bc = 0.0;
-    // branch-free (adding an exact 0.0 leaves a sum unchanged), so the loads
-    // of successive channels pipeline
-#pragma unroll 8
-    for (int i = 0; i < L.n; ++i) {
-      const bool in = sp[i] >= 0.0 && sb[i] == b;
-      bp += in ? sp[i] : 0.0;
-      bc += in ? sc[i] : 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int n = L.n;
+  const int run = (n + 31) / 32;
+  const int i0 = lane * run, i1 = min(n, i0 + run);
+  const double* tp = L.tmp;           // p (< 0: inactive)
+  const double* tc = L.tmp + n;       // capacity
+  const double* tl = L.tmp + 2 * n;   // log2(1 + snr)
+  if (warp == 0) {
+    double loss = 0.0, cap = 0.0, total_w = 0.0;
+    for (int i = i0; i < i1; ++i) {
+      const double p = tp[i];
+      const bool act = p >= 0.0;
+      loss -= act ? tl[i] : 0.0;
+      cap += act ? tc[i] : 0.0;
+      total_w += act ? p : 0.0;
     }
-    op[b] = bp > 0.0 ? 10.0 * log10(bp / 1e-3) : -300.0;
-    oc[b] = bc;
+    loss = warp_sum_fixed(loss);
+    cap = warp_sum_fixed(cap);
+    total_w = warp_sum_fixed(total_w);
+    if (lane == 0) {
+      L.out[4 * n + 0] = loss;
+      L.out[4 * n + 1] = cap;
+      L.out[4 * n + 2] = total_w > 0.0 ? 10.0 * log10(total_w / 1e-3) : -300.0;
+    }
+    return;
   }
-  for (int b = nb + threadIdx.x; b < L.n_bands; b += blockDim.x) {  // beyond kMaxBands
-    op[b] = -300.0;
-    oc[b] = 0.0;
+  double* op = L.out + 4 * n + 3;
+  double* oc = op + L.n_bands;
+  for (int b = warp - 1; b < L.n_bands; b += nw - 1) {
+    double bp = 0.0, bc = 0.0;
+    for (int i = i0; i < i1; ++i) {
+      const bool in = tp[i] >= 0.0 && L.band && L.band[i] == b;
+      bp += in ? tp[i] : 0.0;
+      bc += in ? tc[i] : 0.0;
+    }
+    bp = warp_sum_fixed(bp);
+    bc = warp_sum_fixed(bc);
+    if (lane == 0) {
+      op[b] = bp > 0.0 ? 10.0 * log10(bp / 1e-3) : -300.0;
+      oc[b] = bc;
+    }
   }
-  if (threadIdx.x != 0) return;
-  double loss = 0.0, cap = 0.0, total_w = 0.0;
-#pragma unroll 8
-  for (int i = 0; i < L.n; ++i) {
-    const double p = sp[i];
-    const bool act = p >= 0.0;
-    loss -= act ? sl[i] : 0.0;
-    cap += act ? sc[i] : 0.0;
-    total_w += act ? p : 0.0;
-  }
-  L.out[4 * L.n + 0] = loss;
-  L.out[4 * L.n + 1] = cap;
-  L.out[4 * L.n + 2] = total_w > 0.0 ? 10.0 * log10(total_w / 1e-3) : -300.0;
 }
 
 }  // namespace
@@ -425,12 +427,7 @@ int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_sta
 int run_report(uwb_ctx* c, cudaStream_t st, const LinkDev* Lp = nullptr) {
   LinkDev L = Lp ? *Lp : c->prep->L;
   link_channels_kernel<<<(L.n + 127) / 128, 128, 0, st>>>(L);
-  const size_t smem = static_cast<size_t>(L.n) * (3 * sizeof(double) + sizeof(int));
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      link_totals_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-      static_cast<int>(kMaxOdeChannels * (3 * sizeof(double) + sizeof(int))));
-  (void)attr;
-  link_totals_kernel<<<1, kTotalsThreads, smem, st>>>(L);
+  link_totals_kernel<<<1, kTotalsThreads, 0, st>>>(L);
   c->last_launches += 2;
   cudaEventRecord(c->ev1, st);
   cudaError_t e = cudaGetLastError();
