@@ -33,6 +33,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "nli_kernel.cuh"
 #include "uwb_devmath.cuh"
@@ -263,7 +264,7 @@ __device__ __forceinline__ void mixed_sincos(double x, float* c_out, float* s_ou
 // m >= N (only when N < 16 K) mask p to 0 and feed sincos a 0 angle.
 // HOIST: the lane's K end-edge positions Zr and probe half-logs Hr live in
 // registers for the whole row (single span, K <= 8).
-template <int K, bool FULL, bool HOIST>
+template <int K, bool FULL, bool HOIST, bool TINY>
 __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSmem& S, int idx,
                                                int probe, int sl, unsigned segmask,
                                                const double (&Zr)[K], const double (&Hr)[K]) {
@@ -343,7 +344,13 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
       const double* zm = P.zmid + static_cast<size_t>(k) * NS + sl;
       const double* wd = P.width + static_cast<size_t>(k) * NS + sl;
       // fully unrolled like the fast loop (independent steps interleave);
-      // lanes past N contribute a zero weight
+      // lanes past N contribute a zero weight.  A sinc-branch point has
+      // |phi| w_last <= 1e-4, so its phases are small: TINY kernels are
+      // chosen by the host when 1e-4 z_max / w_last <= 2^-6 (NliParams::
+      // slow_tiny, true for single-span grids like the bench's), and there the
+      // Taylor kernels to x^6 / x^7 are exact to < 1e-19 and replace the
+      // reduction + table sincos (8 FP64 instructions instead of 19).  Each
+      // kernel holds one of the two loops (both in one kernel cost 4 %).
 #pragma unroll
       for (int b = 0; b < K; ++b) {
         const int o = 16 * b;
@@ -362,8 +369,15 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
         const double sinc = fma(x2, fma(x2, 1.0 / 120.0, -1.0 / 6.0), 1.0);
         double w = p * wm * sinc;
         if (!FULL) w = (sl * K + b < N) ? w : 0.0;
+        const double a = phi * __ldg(zm + o);
         double cs, sn;
-        dev_sincos(phi * __ldg(zm + o), &cs, &sn);
+        if constexpr (TINY) {
+          const double a2 = a * a;
+          cs = fma(a2, fma(a2, fma(a2, -1.0 / 720.0, 1.0 / 24.0), -0.5), 1.0);
+          sn = fma(a * a2, fma(a2, fma(a2, -1.0 / 5040.0, 1.0 / 120.0), -1.0 / 6.0), a);
+        } else {
+          dev_sincos(a, &cs, &sn);
+        }
         sre = fma(w, cs, sre);
         sim = fma(w, sn, sim);
       }
@@ -510,7 +524,7 @@ __device__ __forceinline__ double point_kernel_mixed(const NliParams& P, const W
   return re * re + im * im;
 }
 
-template <int K, bool FULL, bool HOIST, bool MIXED>
+template <int K, bool FULL, bool HOIST, bool MIXED, bool TINY>
 __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS : UWB_NLI_MIN_BLOCKS)
     nli_rows_kernel(const NliParams P) {
   __shared__ WarpSmem s_w[kWarps];
@@ -687,7 +701,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
         const int idx = ok ? base + seg : base;
         const double kv =
             MIXED ? point_kernel_mixed<K, FULL, HOIST>(P, S, idx, probe, sl, segmask, Zr, Hr)
-                  : point_kernel<K, FULL, HOIST>(P, S, idx, probe, sl, segmask, Zr, Hr);
+                  : point_kernel<K, FULL, HOIST, TINY>(P, S, idx, probe, sl, segmask, Zr, Hr);
         if (ok && sl == 0) S.kv[S.pt[idx].src] = kv;
       }
       __syncwarp();
@@ -789,38 +803,42 @@ __global__ void finalize_channels_kernel(const FinalizeParams F) {
 using RowKernel = void (*)(const NliParams);
 
 template <int K, bool MIXED>
-RowKernel pick2(int steps, bool one_span) {
+RowKernel pick2(int steps, bool one_span, bool tiny) {
   constexpr bool kHoist = K <= 8;
-  if (one_span && kHoist)
-    return steps == 16 * K ? nli_rows_kernel<K, true, kHoist, MIXED>
-                           : nli_rows_kernel<K, false, kHoist, MIXED>;
-  return steps == 16 * K ? nli_rows_kernel<K, true, false, MIXED>
-                         : nli_rows_kernel<K, false, false, MIXED>;
+  if (one_span && kHoist) {
+    if (!MIXED && tiny)
+      return steps == 16 * K ? nli_rows_kernel<K, true, kHoist, MIXED, !MIXED>
+                             : nli_rows_kernel<K, false, kHoist, MIXED, !MIXED>;
+    return steps == 16 * K ? nli_rows_kernel<K, true, kHoist, MIXED, false>
+                           : nli_rows_kernel<K, false, kHoist, MIXED, false>;
+  }
+  return steps == 16 * K ? nli_rows_kernel<K, true, false, MIXED, false>
+                         : nli_rows_kernel<K, false, false, MIXED, false>;
 }
 
 template <int K>
-RowKernel pick(int steps, bool one_span, bool mixed) {
-  return mixed ? pick2<K, true>(steps, one_span) : pick2<K, false>(steps, one_span);
+RowKernel pick(int steps, bool one_span, bool mixed, bool tiny) {
+  return mixed ? pick2<K, true>(steps, one_span, tiny) : pick2<K, false>(steps, one_span, tiny);
 }
 
-RowKernel row_kernel_for(int steps, bool one_span, bool mixed) {
+RowKernel row_kernel_for(int steps, bool one_span, bool mixed, bool tiny) {
   switch ((steps + 15) / 16) {
-    case 1: return pick<1>(steps, one_span, mixed);
-    case 2: return pick<2>(steps, one_span, mixed);
-    case 3: return pick<3>(steps, one_span, mixed);
-    case 4: return pick<4>(steps, one_span, mixed);
-    case 5: return pick<5>(steps, one_span, mixed);
-    case 6: return pick<6>(steps, one_span, mixed);
-    case 7: return pick<7>(steps, one_span, mixed);
-    case 8: return pick<8>(steps, one_span, mixed);
-    case 9: return pick<9>(steps, one_span, mixed);
-    case 10: return pick<10>(steps, one_span, mixed);
-    case 11: return pick<11>(steps, one_span, mixed);
-    case 12: return pick<12>(steps, one_span, mixed);
-    case 13: return pick<13>(steps, one_span, mixed);
-    case 14: return pick<14>(steps, one_span, mixed);
-    case 15: return pick<15>(steps, one_span, mixed);
-    case 16: return pick<16>(steps, one_span, mixed);
+    case 1: return pick<1>(steps, one_span, mixed, tiny);
+    case 2: return pick<2>(steps, one_span, mixed, tiny);
+    case 3: return pick<3>(steps, one_span, mixed, tiny);
+    case 4: return pick<4>(steps, one_span, mixed, tiny);
+    case 5: return pick<5>(steps, one_span, mixed, tiny);
+    case 6: return pick<6>(steps, one_span, mixed, tiny);
+    case 7: return pick<7>(steps, one_span, mixed, tiny);
+    case 8: return pick<8>(steps, one_span, mixed, tiny);
+    case 9: return pick<9>(steps, one_span, mixed, tiny);
+    case 10: return pick<10>(steps, one_span, mixed, tiny);
+    case 11: return pick<11>(steps, one_span, mixed, tiny);
+    case 12: return pick<12>(steps, one_span, mixed, tiny);
+    case 13: return pick<13>(steps, one_span, mixed, tiny);
+    case 14: return pick<14>(steps, one_span, mixed, tiny);
+    case 15: return pick<15>(steps, one_span, mixed, tiny);
+    case 16: return pick<16>(steps, one_span, mixed, tiny);
     default: return nullptr;
   }
 }
@@ -904,8 +922,8 @@ void allow_row_smem(RowKernel k, int n_r) {
 }
 }  // namespace
 
-int nli_ctas_per_sm(int steps, bool one_span, int n_r, bool mixed) {
-  RowKernel k = row_kernel_for(steps, one_span, mixed);
+int nli_ctas_per_sm(int steps, bool one_span, int n_r, bool mixed, bool tiny) {
+  RowKernel k = row_kernel_for(steps, one_span, mixed, tiny);
   if (!k) return 0;
   allow_row_smem(k, n_r);
   int n = 0;
@@ -921,7 +939,7 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
     const char* e = std::getenv("UWB_NLI_NO_HOIST");
     return e && e[0] == '1';
   }();
-  RowKernel k = row_kernel_for(p.steps, p.n_spans == 1 && !no_hoist, p.mixed != 0);
+  RowKernel k = row_kernel_for(p.steps, p.n_spans == 1 && !no_hoist, p.mixed != 0, p.slow_tiny != 0);
   if (!k || p.n_probes <= 0 || p.col_stride != 16 * ((p.steps + 15) / 16)) return -1;
   int launches = 0;
   cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), stream);

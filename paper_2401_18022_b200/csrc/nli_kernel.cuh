@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <vector>
 
@@ -37,6 +38,8 @@ struct NliParams {
   const double* zmid;     // [n_spans][NS] z_base + mid[m]
   const double* width;    // [n_spans][NS]
   const double* wlast;    // [n_spans] width.back(): fast/slow switch (gn_integral.hpp:156)
+  double zmid_max;        // max |z_mid| over spans: bounds the sinc-branch phase |phi z|
+  int slow_tiny;          // 1: every sinc-branch phase |phi z| <= 2^-6 (slow_tiny_ok)
   double beta2, beta3, beta4;
   // GnSolverConfig
   int n_r;
@@ -81,6 +84,7 @@ struct FinalizeParams {
 // zmid / width / wlast arrays) for a span starting at z_base.
 struct SpanTables {
   std::vector<double> zend, zstart, zmid, width, wlast;
+  double zmid_max = 0.0;  // largest |z| of a step midpoint over all spans
 };
 inline void append_span_tables(const double* edge, const double* mid, const double* width,
                                int steps, double z_base, SpanTables* t) {
@@ -98,6 +102,7 @@ inline void append_span_tables(const double* edge, const double* mid, const doub
   }
   t->zstart.push_back(z_base + edge[0]);
   t->wlast.push_back(width[steps - 1]);
+  for (int m = 0; m < steps; ++m) t->zmid_max = std::max(t->zmid_max, std::fabs(z_base + mid[m]));
 }
 
 // Issue the NLI pipeline on `stream`: queue reset, probe half-log columns,
@@ -108,7 +113,17 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
                cudaEvent_t ev_k0, cudaEvent_t ev_k1);
 
 // CTAs per SM the integrand kernel reaches for a given step count.
-int nli_ctas_per_sm(int steps, bool one_span, int n_r, bool mixed = false);
+int nli_ctas_per_sm(int steps, bool one_span, int n_r, bool mixed = false, bool tiny = false);
+
+// Sinc-branch points have |phi| w_last <= 1e-4 (gn_integral.hpp:156), so their
+// phases satisfy |phi z| <= 1e-4 z_max / w_last; the Taylor sincos of the TINY
+// kernels is exact to < 1e-19 for |phi z| <= 2^-6.
+inline bool slow_tiny_ok(const SpanTables& t) {
+  double wmin = 0.0;
+  for (size_t k = 0; k < t.wlast.size(); ++k)
+    wmin = k == 0 ? t.wlast[k] : std::min(wmin, t.wlast[k]);
+  return wmin > 0.0 && 1e-4 * t.zmid_max <= 0.015625 * wmin;
+}
 constexpr int kMaxSteps = 256;  // 16 lanes x 16 steps per lane
 // Elements allocated past the end of log2rho / zedge / hl2: the integrand's
 // lanes with m >= N load them and mask the result (branch-free tail).

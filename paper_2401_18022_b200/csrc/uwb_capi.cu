@@ -129,6 +129,8 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   P->span_stride = cols;
   P->zedge = d_ze;
   P->zstart = d_zs;
+  P->zmid_max = stb.zmid_max;
+  P->slow_tiny = slow_tiny_ok(stb) ? 1 : 0;
   P->zmid = d_zm;
   P->width = d_wd;
   P->wlast = d_wl;
@@ -214,7 +216,7 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
   }
   cudaEventRecord(c->ev0, st);
   if (np) {
-    const int per_sm = nli_ctas_per_sm(P.steps, P.n_spans == 1, P.n_r, P.mixed != 0);
+    const int per_sm = nli_ctas_per_sm(P.steps, P.n_spans == 1, P.n_r, P.mixed != 0, P.slow_tiny != 0);
     if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
     const int launched = launch_nli(P, F, c->sm_count * per_sm, st, c->evk0, c->evk1);
     if (launched < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");

@@ -290,6 +290,8 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   P.span_stride = 0;
   P.zedge = up(c, c->zedge, st.zend.data(), st.zend.size());
   P.zstart = up(c, c->zstart, st.zstart.data(), st.zstart.size());
+  P.zmid_max = st.zmid_max;
+  P.slow_tiny = slow_tiny_ok(st) ? 1 : 0;
   P.zmid = up(c, c->zmid, st.zmid.data(), st.zmid.size());
   P.width = up(c, c->width, st.width.data(), st.width.size());
   P.wlast = up(c, c->wlast, st.wlast.data(), st.wlast.size());
@@ -385,7 +387,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   L.out = c->report.get<double>(4 * static_cast<size_t>(n) + 3 + 2 * L.n_bands);
   L.tmp = d_tmp;
 
-  const int per_sm = nli_ctas_per_sm(steps, P.n_spans == 1, P.n_r, P.mixed != 0);
+  const int per_sm = nli_ctas_per_sm(steps, P.n_spans == 1, P.n_r, P.mixed != 0, P.slow_tiny != 0);
   if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
   pr->grid_ctas = c->sm_count * per_sm;
   cudaError_t e = cudaStreamSynchronize(c->stream);
