@@ -505,3 +505,37 @@ def test_stress_oband101_matches_reference(name, golden_stress, oracle, engine):
     assert np.array_equal(r.skipped, np.array(rec["skipped"], np.uint8))
     assert _rel(r.eta, rec["eta"]) < NLI_TOL
     assert _rel(np.asarray(r.quadrant).ravel(), np.asarray(rec["quadrant"]).ravel()) < NLI_TOL
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_randomised_configs_vs_oracle(seed, oracle, engine):
+    """Seeded random small configurations against the C oracle (pinned
+    bit-exact to the reference): channel count, spacing, width, centre
+    wavelength, per-channel launch power, n_r, step density (1-13 steps per
+    lane, i.e. hoisted and non-hoisted kernels, FULL and ragged step counts),
+    span count, u1 sampling, Simpson and direct Q4."""
+    rng = np.random.default_rng(1000 + seed)
+    n_ch = int(rng.integers(3, 41))
+    spacing = float(rng.choice([50e9, 75e9, 100e9, 150e9]))
+    lam = float(rng.uniform(1280e-9, 1620e-9))
+    case = Case(n_ch=n_ch, spacing=spacing, bch=spacing * float(rng.uniform(0.6, 0.96)),
+                centre=299792458.0 / lam,
+                launch_w=1e-3 * 10 ** (rng.uniform(-3, 3, n_ch) / 10),
+                n_r=int(rng.integers(6, 48)), density=float(rng.choice([0.25, 0.8, 1.4, 2.5])),
+                span_count=int(rng.integers(1, 4)), length_m=float(rng.choice([50e3, 80e3])),
+                u1_uniform=int(rng.random() < 0.25), simpson=int(rng.random() < 0.25),
+                mirror_q4=int(rng.random() < 0.75), name=f"rand{seed}")
+    from pyoracle import OracleError
+    prep = oracle.prepare(case)
+    grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
+    try:
+        ref = oracle.all_channels_nli(case, prep)
+    except OracleError as exc:  # the reference rejects it: so must the engine, alike
+        assert exc.code == 2
+        with pytest.raises(uwb.ConfigError):
+            uwb.all_channels_nli(grid, spans, betas, None, cfg_of(case), engine=engine, gamma=gamma)
+        return
+    r = uwb.all_channels_nli(grid, spans, betas, None, cfg_of(case), engine=engine, gamma=gamma)
+    assert np.array_equal(r.skipped, ref["skipped"])
+    assert _rel(r.eta, ref["eta"]) < NLI_TOL, case
+    assert _rel(np.asarray(r.quadrant).ravel(), np.asarray(ref["quadrant"]).ravel()) < NLI_TOL
