@@ -539,3 +539,26 @@ def test_randomised_configs_vs_oracle(seed, oracle, engine):
     assert np.array_equal(r.skipped, ref["skipped"])
     assert _rel(r.eta, ref["eta"]) < NLI_TOL, case
     assert _rel(np.asarray(r.quadrant).ravel(), np.asarray(ref["quadrant"]).ravel()) < NLI_TOL
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_randomised_power_evolution_vs_oracle(seed, oracle, engine):
+    """Seeded random combs (3-700 channels: the one-warp and multi-warp
+    channel splits, 1-3 pieces of gain table in range), random launch powers
+    and step densities: the device Raman ODE against the C oracle's
+    restatement of the reference solve (dense mat-vec RK45), 1e-9 in log rho."""
+    rng = np.random.default_rng(2000 + seed)
+    n_ch = int(rng.choice([int(rng.integers(3, 33)), int(rng.integers(33, 97)),
+                           int(rng.integers(97, 701))]))
+    spacing = float(rng.choice([50e9, 75e9, 100e9]))
+    lam = float(rng.uniform(1300e-9, 1600e-9))
+    case = Case(n_ch=n_ch, spacing=spacing, bch=0.9 * spacing, centre=299792458.0 / lam,
+                launch_w=1e-3 * 10 ** (rng.uniform(-4, 4, n_ch) / 10),
+                density=float(rng.choice([0.3, 0.95, 1.4, 2.0])), raman=1, name=f"ode{seed}")
+    ref = oracle.power_evolution(case)
+    grid, fibre = product_scenario(case)
+    zg = uwb.build_distance_grid(case.length_m, case.density)
+    evo = uwb.solve_power_evolution(fibre, grid, zg, uwb.RamanSolveOptions(True), engine=engine)
+    assert evo.steps() == ref["steps"]
+    np.testing.assert_allclose(evo.log_rho, ref["log_rho"], rtol=0, atol=1e-9)
+    np.testing.assert_allclose(evo.rho_end, ref["rho_end"], rtol=1e-9)
