@@ -562,3 +562,31 @@ def test_randomised_power_evolution_vs_oracle(seed, oracle, engine):
     assert evo.steps() == ref["steps"]
     np.testing.assert_allclose(evo.log_rho, ref["log_rho"], rtol=0, atol=1e-9)
     np.testing.assert_allclose(evo.rho_end, ref["rho_end"], rtol=1e-9)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_randomised_evaluate_link_vs_reference(seed, engine):
+    """Full evaluate_link (device ODE + NLI + SNR assembly) on seeded random
+    small combs against the UNMODIFIED reference run here through its harness
+    (oracle/_ref/libuwbref.so; skipped where it was not built)."""
+    from pyoracle import RefLib
+    if not RefLib.available():
+        pytest.skip("oracle/_ref/libuwbref.so not built")
+    R = RefLib()
+    rng = np.random.default_rng(3000 + seed)
+    n_ch = int(rng.integers(5, 41))
+    lam = float(rng.uniform(1290e-9, 1610e-9))
+    case = Case(n_ch=n_ch, spacing=100e9, bch=96e9, centre=299792458.0 / lam,
+                launch_w=1e-3 * 10 ** (rng.uniform(-3, 3, n_ch) / 10),
+                n_r=int(rng.integers(8, 31)), density=float(rng.choice([0.95, 1.4])),
+                span_count=int(rng.integers(1, 3)), name=f"link{seed}")
+    ref = R.evaluate_link(case)
+    grid, fibre = product_scenario(case)
+    lc = uwb.LinkConfig(gn=cfg_of(case), raman=uwb.RamanSolveOptions(True))
+    rep = uwb.evaluate_link(fibre, grid, lc, engine=engine)
+    act = ref["eta"] > 0
+    assert _rel(rep.eta[act], ref["eta"][act]) < 1e-9
+    assert np.max(np.abs(rep.snr_db[act] - ref["snr_db"][act])) < 1e-8
+    np.testing.assert_allclose(rep.p_ase[act], ref["p_ase"][act], rtol=1e-9)
+    assert rep.loss_value == pytest.approx(ref["loss"], rel=1e-9)
+    assert rep.total_capacity == pytest.approx(ref["total_capacity"], rel=1e-9)
