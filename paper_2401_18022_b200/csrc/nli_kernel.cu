@@ -821,6 +821,16 @@ RowKernel pick(int steps, bool one_span, bool mixed, bool tiny) {
   return mixed ? pick2<K, true>(steps, one_span, tiny) : pick2<K, false>(steps, one_span, tiny);
 }
 
+// Long spans (257..512 steps, e.g. 80 km at > 3.2 steps/km): FP64, per-step
+// z / half-log loads (no hoisting at this K); the compensated-FP32 mode stops
+// at 256 steps.
+template <int K>
+RowKernel pick_long(int steps, bool mixed) {
+  if (mixed) return nullptr;
+  return steps == 16 * K ? nli_rows_kernel<K, true, false, false, false>
+                         : nli_rows_kernel<K, false, false, false, false>;
+}
+
 RowKernel row_kernel_for(int steps, bool one_span, bool mixed, bool tiny) {
   switch ((steps + 15) / 16) {
     case 1: return pick<1>(steps, one_span, mixed, tiny);
@@ -839,6 +849,22 @@ RowKernel row_kernel_for(int steps, bool one_span, bool mixed, bool tiny) {
     case 14: return pick<14>(steps, one_span, mixed, tiny);
     case 15: return pick<15>(steps, one_span, mixed, tiny);
     case 16: return pick<16>(steps, one_span, mixed, tiny);
+    case 17: return pick_long<17>(steps, mixed);
+    case 18: return pick_long<18>(steps, mixed);
+    case 19: return pick_long<19>(steps, mixed);
+    case 20: return pick_long<20>(steps, mixed);
+    case 21: return pick_long<21>(steps, mixed);
+    case 22: return pick_long<22>(steps, mixed);
+    case 23: return pick_long<23>(steps, mixed);
+    case 24: return pick_long<24>(steps, mixed);
+    case 25: return pick_long<25>(steps, mixed);
+    case 26: return pick_long<26>(steps, mixed);
+    case 27: return pick_long<27>(steps, mixed);
+    case 28: return pick_long<28>(steps, mixed);
+    case 29: return pick_long<29>(steps, mixed);
+    case 30: return pick_long<30>(steps, mixed);
+    case 31: return pick_long<31>(steps, mixed);
+    case 32: return pick_long<32>(steps, mixed);
     default: return nullptr;
   }
 }

@@ -124,7 +124,7 @@ inline bool slow_tiny_ok(const SpanTables& t) {
     wmin = k == 0 ? t.wlast[k] : std::min(wmin, t.wlast[k]);
   return wmin > 0.0 && 1e-4 * t.zmid_max <= 0.015625 * wmin;
 }
-constexpr int kMaxSteps = 256;  // 16 lanes x 16 steps per lane
+constexpr int kMaxSteps = 512;  // 16 lanes x 32 steps per lane
 // Elements allocated past the end of log2rho / zedge / hl2: the integrand's
 // lanes with m >= N load them and mask the result (branch-free tail).
 constexpr int kTablePad = 32;

@@ -66,7 +66,7 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
       return fail(UWB_CONFIG_ERROR, "nli_psd_at: span evolution does not match the channel grid");
   }
   if (steps < 1 || steps > kMaxSteps)
-    return fail(UWB_CONFIG_ERROR, "uwb: distance steps per span must be in [1, 256]");
+    return fail(UWB_CONFIG_ERROR, "uwb: distance steps per span must be in [1, 512]");
 
   // Padded device layout (nli_kernel.cuh): columns NS = 16 ceil(N/16) long,
   // one zero pad column n per span, edges past N repeat the span end.

@@ -236,7 +236,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   if ((rc = distance_grid_host(fb->length_m, lk->density, &edge, &mid, &width))) return rc;
   const int steps = static_cast<int>(mid.size());
   if (steps > kMaxSteps)
-    return fail(UWB_CONFIG_ERROR, "uwb: distance steps per span must be in [1, 256]");
+    return fail(UWB_CONFIG_ERROR, "uwb: distance steps per span must be in [1, 512]");
   const int n = g->n_ch;
   release_link_state(c);
   auto* pr = new uwb_ctx::Prepared();

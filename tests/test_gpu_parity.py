@@ -590,3 +590,20 @@ def test_randomised_evaluate_link_vs_reference(seed, engine):
     np.testing.assert_allclose(rep.p_ase[act], ref["p_ase"][act], rtol=1e-9)
     assert rep.loss_value == pytest.approx(ref["loss"], rel=1e-9)
     assert rep.total_capacity == pytest.approx(ref["total_capacity"], rel=1e-9)
+
+
+@pytest.mark.parametrize("density", [3.5, 6.0])
+def test_long_spans_vs_oracle(density, oracle, engine):
+    """More than 256 distance steps per span (the K = 17..32 kernels): 80 km at
+    3.5 and 6.0 steps/km (281 / 481 steps), against the oracle at 1e-9."""
+    case = oband11(n_r=24, density=density, name=f"long{density}")
+    prep = oracle.prepare(case)
+    assert prep["spans"][0]["steps"] > 256
+    ref = oracle.all_channels_nli(case, prep)
+    grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
+    r = uwb.all_channels_nli(grid, spans, betas, None, cfg_of(case), engine=engine, gamma=gamma)
+    assert _rel(r.eta, ref["eta"]) < NLI_TOL
+    # and the full device path (ODE writes the K > 16 lane layout)
+    g2, fibre = product_scenario(case)
+    rep = uwb.evaluate_link(fibre, g2, uwb.LinkConfig(gn=cfg_of(case)), engine=engine)
+    assert _rel(rep.eta, ref["eta"]) < 1e-8
