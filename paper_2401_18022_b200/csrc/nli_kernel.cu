@@ -33,7 +33,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
-#include <type_traits>
 
 #include "nli_kernel.cuh"
 #include "uwb_devmath.cuh"
