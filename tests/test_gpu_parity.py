@@ -565,6 +565,24 @@ def test_randomised_power_evolution_vs_oracle(seed, oracle, engine):
     np.testing.assert_allclose(evo.rho_end, ref["rho_end"], rtol=1e-9)
 
 
+@pytest.mark.parametrize("n_ch", [800, 1500])
+def test_wide_comb_power_evolution_vs_oracle(n_ch, oracle, engine):
+    """Combs beyond 256 ODE threads (the 512-thread CTA: 9 and 16 warps of 3
+    channels, the rolled cross-warp offsets) against the oracle, 1e-9 in
+    log rho."""
+    rng = np.random.default_rng(4000 + n_ch)
+    case = Case(n_ch=n_ch, spacing=25e9, bch=22e9, centre=299792458.0 / 1450e-9,
+                launch_w=1e-4 * 10 ** (rng.uniform(-3, 3, n_ch) / 10),
+                density=0.3, raman=1, name=f"wide{n_ch}")
+    ref = oracle.power_evolution(case)
+    grid, fibre = product_scenario(case)
+    zg = uwb.build_distance_grid(case.length_m, case.density)
+    evo = uwb.solve_power_evolution(fibre, grid, zg, uwb.RamanSolveOptions(True), engine=engine)
+    assert evo.steps() == ref["steps"]
+    np.testing.assert_allclose(evo.log_rho, ref["log_rho"], rtol=0, atol=1e-9)
+    np.testing.assert_allclose(evo.rho_end, ref["rho_end"], rtol=1e-9)
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_randomised_evaluate_link_vs_reference(seed, engine):
     """Full evaluate_link (device ODE + NLI + SNR assembly) on seeded random
