@@ -150,7 +150,7 @@ def run_reference(args):
     fn, kind = reference_eval_fn(args.n_r, args.density)
     # each step is one full evaluation (~5-10 s on 8-16 host cores): bound the run
     steps = max(1, min(args.steps, 5))
-    warm = min(args.warmup, 1)
+    warm = max(1, min(args.warmup, 3))
     for _ in range(warm):
         fn()
     ts, parts = [], []
