@@ -143,14 +143,18 @@ def reference_eval_fn(n_r, density):
     return (lambda: O.evaluate_link(case)), "port"
 
 
+# each reference step is one full evaluation (~5 s on 16 host cores): the arm
+# honours --steps / --warmup up to these caps (the driver's 20 / 5 fit: ~2 min)
+REF_MAX_STEPS, REF_MAX_WARMUP = 30, 5
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
     fn, kind = reference_eval_fn(args.n_r, args.density)
-    # each step is one full evaluation (~5-10 s on 8-16 host cores): bound the run
-    steps = max(1, min(args.steps, 5))
-    warm = max(1, min(args.warmup, 3))
+    steps = max(1, min(args.steps, REF_MAX_STEPS))
+    warm = max(1, min(args.warmup, REF_MAX_WARMUP))
     for _ in range(warm):
         fn()
     ts, parts = [], []
@@ -165,6 +169,10 @@ def run_reference(args):
             "steps": steps, "warmup": warm, "ms_per_step": v * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config(args, 1),
+            "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "capped": (steps != args.steps or warm != args.warmup),
+            "result_check": {"loss": float(r["loss"]),
+                             "total_capacity_tbps": float(r["total_capacity"]) / 1e12},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                              "sample": f"{steps} full evaluate_link calls (ODE+NLI+SNR), "
                                        f"workers=all {cores} host threads",
@@ -175,6 +183,31 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------- engine
+def headline_parity(rep, n, args):
+    """Max deviation of the timed evaluation's report from the reference's own
+    evaluate_link at the same configuration (tests/golden/golden_headline.npz,
+    written from the unmodified reference by tests/golden/make_golden_headline.py).
+    Only the default workload (589 ch, 150 / 1.4, 0 dBm) has a fixture."""
+    if (args.n_r, args.density) != (150, 1.4):
+        return None
+    gdir = os.path.join(ROOT, "tests", "golden")
+    try:
+        arr = np.load(os.path.join(gdir, "golden_headline.npz"))
+        with open(os.path.join(gdir, "golden_headline.json")) as fh:
+            meta = json.load(fh)["evaluate_link"]["uwb589_150_1.4"]
+    except (OSError, KeyError) as e:
+        return {"error": str(e)}
+    eta_ref, snr_ref = arr["uwb589_150_1.4/eta"], arr["uwb589_150_1.4/snr_db"]
+    act = eta_ref > 0
+    eta, snr = rep[:n], rep[2 * n:3 * n]
+    return {"max_rel_eta": float(np.max(np.abs(eta[act] - eta_ref[act]) / eta_ref[act])),
+            "max_abs_dsnr_db": float(np.max(np.abs(snr[act] - snr_ref[act]))),
+            "rel_loss": float(abs(rep[4 * n] / meta["loss"] - 1.0)),
+            "skip_set_equal": bool(np.array_equal(eta > 0, act)),
+            "against": "reference evaluate_link, tests/golden/golden_headline.npz",
+            "tolerance": {"max_rel_eta": 1e-9, "max_abs_dsnr_db": 1e-8}}
+
+
 def read_traffic():
     p = os.path.join(ROOT, "profiles", "nli_traffic.json")
     if os.path.exists(p):
@@ -440,6 +473,7 @@ def run_engine(args):
             "gpu_launches": int(launches),
             "variants": variants,
             "result_check": {"loss": float(rep[4 * n]), "total_capacity_tbps": float(rep[4 * n + 1]) / 1e12},
+            "parity": headline_parity(rep, n, args),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -154,7 +154,12 @@ int uwb_device_info(uwb_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor);
 int uwb_set_channel_subset(uwb_ctx* ctx, int n, const int* channels);
 
 /* all_channels_nli (gn_integral.hpp:334-363): gamma[n_ch] = gamma_at per
- * channel (:353).  Spans must share one step count. */
+ * channel (:353).  Spans must share one step count.  Like the reference, the
+ * NLI entry points do not run ChannelGrid::validate (the reference never
+ * calls it on this path); they reject only what would make the device's index
+ * arithmetic undefined.  uwb_power_evolution / uwb_evaluate_link /
+ * uwb_evaluate_link_prepare run the full ChannelGrid::validate
+ * (channel_grid.hpp:44-61) as solve_power_evolution does (raman_power.hpp:56). */
 int uwb_all_channels_nli(uwb_ctx* ctx, const uwb_grid* grid, int n_spans, const uwb_span* spans,
                          const double beta[3], const double* gamma, const uwb_nli_cfg* cfg,
                          uwb_nli_result* out);
@@ -194,12 +199,29 @@ int uwb_evaluate_link(uwb_ctx* ctx, const uwb_grid* grid, const uwb_fibre* fibre
  * `value` leg: static state (grid layout, fibre, configs) is uploaded by
  * uwb_evaluate_link_prepare once; each uwb_evaluate_link_resident call takes
  * launch powers already in device memory (psd_dev [n_ch], W/Hz) and leaves the
- * report in device memory (report_dev: [n_ch*4] = eta|p_ase|snr_db|capacity
- * followed by [3] totals).  stream: cudaStream_t or NULL for the context's. */
+ * report in device memory.  stream: cudaStream_t or NULL for the context's.
+ *
+ * Report layout (report_dev here, and each row of uwb_evaluate_link_many's
+ * report_host), report_len = 4*n_ch + 3 + 2*n_bands doubles:
+ *   [0, n_ch)               eta      1/W^2 (0 for skipped channels)
+ *   [n_ch, 2 n_ch)          p_ase    W
+ *   [2 n_ch, 3 n_ch)        snr_db
+ *   [3 n_ch, 4 n_ch)        capacity b/s
+ *   [4 n_ch + 0..2]         loss_value, total_capacity, total_power_dbm
+ *   [4 n_ch + 3, +n_bands)  band_power_dbm
+ *   [.. + n_bands, +n_bands) band_capacity
+ * (n_bands = uwb_link_cfg::n_bands of the prepare call; uwb_report_len
+ * returns report_len.)
+ *
+ * The skip set is re-derived from each call's launch profile, like the
+ * reference (guard or psd <= 0, gn_integral.hpp:349-352): a channel that was
+ * dark at prepare time and is lit in a later call gets its NLI. */
 int uwb_evaluate_link_prepare(uwb_ctx* ctx, const uwb_grid* grid, const uwb_fibre* fibre,
                               const uwb_link_cfg* link, const uwb_nli_cfg* cfg);
 int uwb_evaluate_link_resident(uwb_ctx* ctx, const double* psd_dev, double* report_dev,
                                void* stream);
+/* Doubles per report of the prepared link (see the layout above). */
+int uwb_report_len(uwb_ctx* ctx, int* len);
 /* n_eval full evaluations of the prepared link back to back on the device
  * (optimise_launch_powers' value + forward-difference gradient calls,
  * link_optimizer.hpp:294-309): psd_host [n_eval][n_ch] launch PSDs (W/Hz) in,

@@ -118,6 +118,7 @@ SIGNATURES = {
     "uwb_evaluate_link_resident_noise": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "uwb_evaluate_link_resident_report": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "uwb_link_eta_buffer": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), IP]),
+    "uwb_report_len": (C.c_int, [C.c_void_p, IP]),
     "uwb_resident_status": (C.c_int, [C.c_void_p]),
     "uwb_last_transfer_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_ulonglong),
                                           C.POINTER(C.c_ulonglong)]),

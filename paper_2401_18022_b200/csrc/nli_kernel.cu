@@ -622,6 +622,12 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
     row = __shfl_sync(kFull, row, 0);
     if (row >= P.total_rows) break;
     const int probe = row / per_probe;
+    // prepared path: the probe's channel is dark in this evaluation -> the
+    // reference skips it (gn_integral.hpp:349-352); its rows add nothing
+    if (P.probe_chan && !(__ldg(P.psd + __ldg(P.probe_chan + probe)) > 0.0)) {
+      if (lane == 0) P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
+      continue;
+    }
     if (HOIST && probe != cur_probe) {
       cur_probe = probe;
 #pragma unroll
@@ -845,7 +851,9 @@ __global__ void finalize_channels_kernel(const FinalizeParams F) {
   const int ch = blockIdx.x * blockDim.x + threadIdx.x;
   if (ch >= F.n_ch) return;
   const int p0 = F.chan_probe0[ch];
-  if (p0 < 0) {
+  // p0 < 0: not probed (guard, outside the subset, or dark at the call);
+  // psd <= 0 with a probe: dark in this evaluation of a prepared link
+  if (p0 < 0 || !(F.psd[ch] > 0.0)) {
     F.eta[ch] = F.nli_psd[ch] = F.nli_power[ch] = 0.0;
     for (int q = 0; q < 4; ++q) F.quad[4 * ch + q] = 0.0;
     F.skipped[ch] = 1;

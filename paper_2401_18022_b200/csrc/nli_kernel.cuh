@@ -49,6 +49,11 @@ struct NliParams {
   // probes
   int n_probes;
   const double* probe_nu;  // [n_probes]
+  // [n_probes] channel of each probe, or null.  When set (the prepared /
+  // resident path), rows of a probe whose channel has psd <= 0 in this
+  // evaluation are skipped on the device: the reference's per-call skip set
+  // (gn_integral.hpp:349-352) re-derived from the launch profile.
+  const int* probe_chan;
   double* hl2;             // [n_probes][n_spans][NS] 16 x log2 half-power of the probe
   // work queue + outputs
   int total_rows;               // n_probes * n_q * n_r

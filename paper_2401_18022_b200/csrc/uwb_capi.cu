@@ -37,7 +37,13 @@ int cuda_fail(cudaError_t e, const char* what) {
   return set_err(UWB_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// Validate the grid as ChannelGrid::validate does (channel_grid.hpp:44-61).
+// Grid checks of the NLI entry points (all_channels_nli / nli_psd_at /
+// channel_nli).  The reference does NOT call ChannelGrid::validate on that
+// path (gn_integral.hpp:218-363): psd_at and stencil_for simply assume the
+// equal spacing, and so does the device.  These are the checks that keep the
+// device's index arithmetic defined (non-empty, positive spacing/width,
+// ascending, no negative PSD); the ODE and link entry points run the full
+// ChannelGrid::validate (validate_grid_full) exactly where the reference does.
 int validate_grid(const uwb_grid* g) {
   if (!g || g->n_ch < 1 || !g->freq || !g->psd || !g->guard)
     return fail(UWB_CONFIG_ERROR, "channel grid is empty");
@@ -49,6 +55,31 @@ int validate_grid(const uwb_grid* g) {
     if (i > 0 && !(g->freq[i] > g->freq[i - 1]))
       return fail(UWB_CONFIG_ERROR, "grid must ascend in frequency");
   }
+  return UWB_OK;
+}
+
+// ChannelGrid::validate (channel_grid.hpp:44-61), every check in the
+// reference's order: solve_power_evolution calls it first (raman_power.hpp:56),
+// so uwb_power_evolution, uwb_evaluate_link and uwb_evaluate_link_prepare do
+// too.  The device ODE's separable coupling relies on the equal spacing
+// (raman_ode.cu: f_j - f_i = (j - i) spacing).
+int validate_grid_full(const uwb_grid* g) {
+  if (!g || g->n_ch < 1 || !g->freq || !g->psd || !g->guard)
+    return fail(UWB_CONFIG_ERROR, "channel grid is empty");
+  if (!(g->spacing > 0.0) || !(g->bch > 0.0))
+    return fail(UWB_CONFIG_ERROR, "grid spacing and width must be > 0");
+  if (g->bch > g->spacing + 1e-9) return fail(UWB_CONFIG_ERROR, "channel width exceeds spacing");
+  for (int i = 0; i < g->n_ch; ++i) {
+    if (g->psd[i] < 0.0) return fail(UWB_CONFIG_ERROR, "negative launch PSD");
+    if (i > 0 && !(g->freq[i] > g->freq[i - 1]))
+      return fail(UWB_CONFIG_ERROR, "grid must ascend in frequency");
+    if (i > 0 && std::abs((g->freq[i] - g->freq[i - 1]) - g->spacing) > 1e-3)
+      return fail(UWB_CONFIG_ERROR, "grid must be equally spaced");
+  }
+  const double need = std::max(std::abs(g->freq[0] - g->centre),
+                               std::abs(g->freq[g->n_ch - 1] - g->centre)) + 0.5 * g->bch;
+  if (g->half_band + 1e-3 < need)
+    return fail(UWB_CONFIG_ERROR, "half_band smaller than occupied hull");
   return UWB_OK;
 }
 
@@ -247,25 +278,31 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
 }
 
 // Probe list of all_channels_nli (gn_integral.hpp:348-353, channel_nli :316-329).
+// include_dark: also probe non-guard channels with psd <= 0 (the prepared
+// path, whose device kernels re-derive the skip set per evaluation);
+// probe_chan (may be null) receives each probe's channel.
 void channel_probes(const uwb_grid* g, const double* gamma, const uwb_nli_cfg* cfg,
                     const std::vector<int>& subset, std::vector<double>* nu,
-                    std::vector<double>* gam, std::vector<int>* chan_probe0) {
+                    std::vector<double>* gam, std::vector<int>* chan_probe0, bool include_dark,
+                    std::vector<int>* probe_chan) {
   const int n = g->n_ch;
   std::vector<uint8_t> want(n, subset.empty() ? 1 : 0);
   for (int ch : subset)
     if (ch >= 0 && ch < n) want[ch] = 1;
   chan_probe0->assign(n, -1);
   for (int ch = 0; ch < n; ++ch) {
-    if (!want[ch] || g->guard[ch] || g->psd[ch] <= 0.0) continue;
+    if (!want[ch] || g->guard[ch] || (!include_dark && g->psd[ch] <= 0.0)) continue;
     (*chan_probe0)[ch] = static_cast<int>(nu->size());
     const double f = g->freq[ch];
+    const int np = cfg->simpson ? 3 : 1;
     nu->push_back(f);
-    gam->push_back(gamma[ch]);
     if (cfg->simpson) {
       nu->push_back(f - 0.5 * g->bch);
-      gam->push_back(gamma[ch]);
       nu->push_back(f + 0.5 * g->bch);
+    }
+    for (int k = 0; k < np; ++k) {
       gam->push_back(gamma[ch]);
+      if (probe_chan) probe_chan->push_back(ch);
     }
   }
 }

@@ -31,13 +31,15 @@ inline cudaError_t xfer_sync(uwb_ctx* c, void* dst, const void* src, size_t byte
 inline void reset_xfer(uwb_ctx* c) { c->h2d_bytes = c->d2h_bytes = 0; }
 int cuda_fail(cudaError_t e, const char* what);
 int validate_grid(const uwb_grid* g);
+int validate_grid_full(const uwb_grid* g);
 int set_cfg(const uwb_nli_cfg* cfg, NliParams* P, int precision);
 int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vector<double>& nu,
                const std::vector<double>& gam, const std::vector<int>* chan_probe0,
                bool sync_stats);
 void channel_probes(const uwb_grid* g, const double* gamma, const uwb_nli_cfg* cfg,
                     const std::vector<int>& subset, std::vector<double>* nu,
-                    std::vector<double>* gam, std::vector<int>* chan_probe0);
+                    std::vector<double>* gam, std::vector<int>* chan_probe0,
+                    bool include_dark = false, std::vector<int>* probe_chan = nullptr);
 int launch_finalize_channels_only(const FinalizeParams& f, cudaStream_t st);
 void release_link_state(uwb_ctx* c);
 int distance_grid_host(double length_m, double density, std::vector<double>* edge,

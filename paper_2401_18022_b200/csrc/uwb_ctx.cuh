@@ -59,7 +59,7 @@ struct uwb_ctx {
   // spans
   uwb::DBuf log2rho, zedge, zstart, zmid, width, wlast;
   // probes + work
-  uwb::DBuf probe_nu, probe_gamma, hl2, rowsum, counter, n_eval, probe_g, probe_quad, chan_probe0;
+  uwb::DBuf probe_nu, probe_chan, probe_gamma, hl2, rowsum, counter, n_eval, probe_g, probe_quad, chan_probe0;
   // per-channel results
   uwb::DBuf eta, nli_psd, nli_power, quad, skipped;
   // uwb_evaluate_link_many: the batch's launch profiles and reports

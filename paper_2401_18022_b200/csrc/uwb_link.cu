@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -224,7 +225,10 @@ namespace {
 
 int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_cfg* lk,
             const uwb_nli_cfg* cfg) {
-  int rc = validate_grid(g);
+  // the buffers below are shared with the previous prepared link: it is gone
+  // from here on, and the new one is published only once complete
+  release_link_state(c);
+  int rc = validate_grid_full(g);  // solve_power_evolution's grid.validate() (raman_power.hpp:56)
   if (rc) return rc;
   if (!fb || !lk || !cfg) return fail(UWB_CONFIG_ERROR, "missing fibre / link / solver config");
   if (!fb->alpha || !fb->aeff || !fb->gamma || !lk->nf_db)
@@ -238,9 +242,8 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   if (steps > kMaxSteps)
     return fail(UWB_CONFIG_ERROR, "uwb: distance steps per span must be in [1, 512]");
   const int n = g->n_ch;
-  release_link_state(c);
-  auto* pr = new uwb_ctx::Prepared();
-  c->prep = pr;
+  std::unique_ptr<uwb_ctx::Prepared> owner(new uwb_ctx::Prepared());
+  uwb_ctx::Prepared* pr = owner.get();
   pr->n = n;
   pr->steps = steps;
   pr->span_count = fb->span_count;
@@ -301,10 +304,18 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   c->last_steps = steps;
   c->last_spans = fb->span_count;
 
-  // probes: channels with launch power (the resident path keeps this set)
+  // Probes: every non-guard channel of the subset, lit or dark.  The
+  // reference re-derives its skip set (guard or psd <= 0, gn_integral.hpp:
+  // 349-352) on every call; the resident path takes a new launch profile per
+  // call, so the device re-derives it too: rows of a probe whose channel is
+  // dark in THIS evaluation exit at once (NliParams::probe_chan) and
+  // finalize_channels_kernel reports the channel skipped.  A channel dark at
+  // prepare time may therefore light up later and gets its NLI.  (The grid is
+  // validated, so every channel lies inside the half band: no quadrant_limits
+  // error can depend on the launch profile.)
   std::vector<double> nu, gam;
-  std::vector<int> cp;
-  channel_probes(g, fb->gamma, cfg, c->subset, &nu, &gam, &cp);
+  std::vector<int> cp, pch;
+  channel_probes(g, fb->gamma, cfg, c->subset, &nu, &gam, &cp, /*include_dark=*/true, &pch);
   for (double v : nu)
     if (std::abs(v - g->centre) > g->half_band)
       return fail(UWB_CONFIG_ERROR, "quadrant_limits: channel offset must lie inside the half band");
@@ -312,6 +323,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   P.n_probes = np;
   P.total_rows = np * P.n_q * P.n_r;
   P.probe_nu = up(c, c->probe_nu, nu.data(), nu.size());
+  P.probe_chan = up(c, c->probe_chan, pch.data(), pch.size());
   P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * NS);
   P.rowsum = c->rowsum.get<double>(std::max(P.total_rows, 1));
   P.counter = c->counter.get<unsigned int>(1);
@@ -390,8 +402,15 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   const int per_sm = nli_ctas_per_sm(steps, P.n_spans == 1, P.n_r, P.mixed != 0, P.slow_tiny != 0);
   if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
   pr->grid_ctas = c->sm_count * per_sm;
+  if (!P.log2rho || !P.zedge || !P.zstart || !P.zmid || !P.width || !P.wlast || !P.probe_nu ||
+      !P.probe_chan || !P.hl2 || !P.rowsum || !P.counter || !P.n_eval || !F.probe_gamma ||
+      !F.probe_g || !F.probe_quad || !F.chan_probe0 || !F.eta || !F.nli_psd || !F.nli_power ||
+      !F.quad || !F.skipped || !L.out || !d_freq || !pr->d_psd || !d_guard || !d_alpha ||
+      !pr->d_aeff || !d_nf || !d_mid)
+    return fail(UWB_CUDA_ERROR, "device allocation failed");
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cuda_fail(e, "prepare");
+  c->prep = owner.release();  // complete: publish
   return UWB_OK;
 }
 
@@ -474,6 +493,7 @@ int uwb_evaluate_link_prepare(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre*
 int uwb_evaluate_link_resident(uwb_ctx* c, const double* psd_dev, double* report_dev,
                                void* stream) {
   if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
+  cudaSetDevice(c->device);
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
   reset_xfer(c);
   int rc = run_prepared(c, psd_dev, st);
@@ -634,12 +654,14 @@ int uwb_evaluate_link(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
 
 int uwb_evaluate_link_resident_noise(uwb_ctx* c, const double* psd_dev, void* stream) {
   if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
+  cudaSetDevice(c->device);
   reset_xfer(c);
   return run_noise(c, psd_dev, stream ? static_cast<cudaStream_t>(stream) : c->stream);
 }
 
 int uwb_evaluate_link_resident_report(uwb_ctx* c, double* report_dev, void* stream) {
   if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
+  cudaSetDevice(c->device);
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
   c->last_launches = 0;
   int rc = run_report(c, st);
@@ -648,6 +670,12 @@ int uwb_evaluate_link_resident_report(uwb_ctx* c, double* report_dev, void* stre
     const size_t cnt = 4 * static_cast<size_t>(c->prep->n) + 3 + 2 * c->prep->L.n_bands;
     xfer(c, report_dev, c->prep->L.out, cnt * sizeof(double), cudaMemcpyDeviceToDevice, st);
   }
+  return UWB_OK;
+}
+
+int uwb_report_len(uwb_ctx* c, int* len) {
+  if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
+  if (len) *len = 4 * c->prep->n + 3 + 2 * c->prep->L.n_bands;
   return UWB_OK;
 }
 
@@ -684,7 +712,7 @@ int uwb_power_evolution(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre
   cudaSetDevice(c->device);
   release_link_state(c);  // shares buffers with the prepared evaluation
   reset_xfer(c);
-  int rc = validate_grid(grid);
+  int rc = validate_grid_full(grid);  // raman_power.hpp:56
   if (rc) return rc;
   if (!fibre || !link || !fibre->alpha || !fibre->aeff)
     return fail(UWB_CONFIG_ERROR, "missing fibre arrays");

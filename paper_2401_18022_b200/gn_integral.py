@@ -574,7 +574,9 @@ class ResidentLink:
         self._g = g
         N.check(self.eng.lib.uwb_evaluate_link_prepare(self.eng.h, N.C.byref(g), N.C.byref(fc),
                                                        N.C.byref(lk), N.C.byref(c)))
-        self.report_len = 4 * self.n + 3 + 2 * N_BANDS
+        rl = N.C.c_int()
+        N.check(self.eng.lib.uwb_report_len(self.eng.h, N.C.byref(rl)))
+        self.report_len = rl.value  # 4 n + 3 + 2 n_bands (include/uwb_nli.h)
 
     def run(self, psd_dev_ptr: int, report_dev_ptr: int, stream_ptr: int = 0):
         """ODE + NLI + SNR assembly for the launch PSD at psd_dev_ptr."""
