@@ -9,6 +9,7 @@ page back to the .cu files.
 """
 from __future__ import annotations
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -40,28 +41,51 @@ def needs_build():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def compile_link(out, extra=(), verbose=False):
+OBJ_DIR = os.path.join(os.path.dirname(PKG), "build", "obj")
+
+
+def _headers():
+    hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    inc = os.path.join(PKG, "..", "include")
+    hs += [os.path.join(inc, f) for f in ("uwb_nli.h", "uwb_model.h")]
+    return [h for h in hs if os.path.exists(h)]
+
+
+def compile_link(out, extra=(), verbose=False, cache=True):
     """One nvcc -c per source in parallel (the template instantiations make
-    each file slow on its own), then one shared-library link."""
+    each file slow on its own), then one shared-library link.  With `cache`,
+    objects live in build/obj (git-ignored) and a source is recompiled only
+    when it, a header or the flags changed."""
     from concurrent.futures import ThreadPoolExecutor
 
-    objs = [out + "." + os.path.splitext(src)[0] + ".o" for src in SOURCES]
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    tag = hashlib.sha1(" ".join(ARCH + FLAGS + list(extra)).encode()).hexdigest()[:8]
+    objs = [os.path.join(OBJ_DIR, os.path.splitext(src)[0] + "." + tag + ".o") for src in SOURCES]
+    hdr_t = max(os.path.getmtime(h) for h in _headers())
+
+    def stale(src, obj):
+        if not cache or not os.path.exists(obj):
+            return True
+        t = os.path.getmtime(obj)
+        return t < os.path.getmtime(os.path.join(CSRC, src)) or t < hdr_t
 
     def cc(args):
         src, obj = args
-        cmd = [nvcc()] + ARCH + FLAGS + list(extra) + ["-c", "-o", obj, os.path.join(CSRC, src)]
+        if not stale(src, obj):
+            return subprocess.CompletedProcess([], 0, "", "")
+        cmd = [nvcc()] + ARCH + FLAGS + list(extra) + ["-c", "-o", obj + ".tmp", os.path.join(CSRC, src)]
         if verbose:
             print(" ".join(cmd), flush=True)
-        return subprocess.run(cmd, capture_output=True, text=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode == 0:
+            os.replace(obj + ".tmp", obj)
+        return r
 
     with ThreadPoolExecutor(len(SOURCES)) as ex:
         results = list(ex.map(cc, zip(SOURCES, objs)))
     link = [nvcc()] + ARCH + ["-shared", "-o", out] + objs
     results.append(subprocess.run(link, capture_output=True, text=True)
                    if all(r.returncode == 0 for r in results) else None)
-    for o in objs:
-        if os.path.exists(o):
-            os.remove(o)
     for r in results:
         if r is None:
             continue

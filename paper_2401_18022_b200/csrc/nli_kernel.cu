@@ -138,13 +138,14 @@ __constant__ double c_e4[6] = {kE4c1, kE4c2, kE4c3, kE4c4, kE4c5, kE4c6};
 // the 11-channel goldens (tests: 1e-9; north star: 1e-6).
 __constant__ double c_e5f[5] = {0.04332169878499661, 0.0009383847926296655, 1.3550807777515591e-05,
                                 1.4676387236639375e-07, 1.2716084569825118e-09};
-__constant__ double c_s3f[3] = {-0.166666666661735, 0.008333331030608612, -0.0001982534004245333};
+__constant__ double c_s3f[3] = {kStepS0, kStepS1, kStepS2};
 __constant__ double c_c4f[4] = {-0.4999999999999954, 0.0416666666627131, -0.0013888883764931453,
                                 2.478033379585741e-05};
 #if UWB_FAST_POLY >= 2
-__constant__ double c_e4f[4] = {0.043321698775062166, 0.0009383847926296648, 1.3551125679628034e-05,
-                                1.4676387236979493e-07};
-__constant__ double c_c3f[3] = {-0.4999999999556206, 0.04166664594464585, -0.0013874553368951438};
+// the step kernels' coefficients live in uwb_devmath.cuh (kStep*), where
+// tests/test_devmath.py checks them on the host
+__constant__ double c_e4f[4] = {kStepE0, kStepE1, kStepE2, kStepE3};
+__constant__ double c_c3f[3] = {kStepC0, kStepC1, kStepC2};
 #endif
 
 // 2^(j/16) for dev_exp2_16, filled by each CTA at start.  A file-scope

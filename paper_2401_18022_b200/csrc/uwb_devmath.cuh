@@ -301,4 +301,56 @@ UWB_HD void sincos_tab16(double x, const double* cos16, const double* sin16, dou
   *s_out = fmad(sin16[q], cr, cos16[q] * sr);
 }
 
+// ---- step kernels of the integrand's hot loop (nli_kernel.cu, UWB_FAST_POLY=2)
+// Shorter than the ulp-accurate kernels above: they only enter the per-step
+// phasor sums, never a discrete decision (the row setup keeps exp2_16).
+// Chebyshev fits in 50-digit arithmetic on the reduced ranges:
+//   2^(r/16), |r| <= 1/2: 1 + r P(r), P degree 3 (quartic)  max rel. error 5e-12
+//   sin r, |r| <= pi/16:  r + r^3 S(r^2), S degree 2        max abs. error 3.7e-14
+//   cos r, |r| <= pi/16:  1 + r^2 C(r^2), C degree 2        max abs. error 1.7e-12
+// nli_kernel.cu copies these into __constant__ banks (c_e4f, c_s3f, c_c3f);
+// tests/test_devmath.py checks the restatements below against long double.
+constexpr double kStepE0 = 0.043321698775062166;
+constexpr double kStepE1 = 0.0009383847926296648;
+constexpr double kStepE2 = 1.3551125679628034e-05;
+constexpr double kStepE3 = 1.4676387236979493e-07;
+constexpr double kStepS0 = -0.166666666661735;
+constexpr double kStepS1 = 0.008333331030608612;
+constexpr double kStepS2 = -0.0001982534004245333;
+constexpr double kStepC0 = -0.4999999999556206;
+constexpr double kStepC1 = 0.04166664594464585;
+constexpr double kStepC2 = -0.0013874553368951438;
+
+// nli_kernel.cu step_exp2_16 (same operation sequence).
+UWB_HD double step_exp2_16(double x, const double* tab16) {
+  const double t = x + kMagic;
+  const int k = lo_word(t);
+  const double r = x - (t - kMagic);
+  double p = fmad(r, kStepE3, kStepE2);
+  p = fmad(p, r, kStepE1);
+  p = fmad(p, r, kStepE0);
+  p = fmad(p, r, 1.0);
+  const double s = tab16[k & 15] * p;
+  return from_words(hi_word(s) + ((k >> 4) << 20), lo_word(s));
+}
+
+// nli_kernel.cu dev_sincos_table at UWB_FAST_POLY=2 (same operation sequence).
+UWB_HD void step_sincos_tab16(double x, const double* cos16, const double* sin16, double* c_out,
+                              double* s_out) {
+  const double t = fmad(x, kEightOverPi, kMagic);
+  const int q = lo_word(t) & 15;
+  const double kd = t - kMagic;
+  double r = fmad(kd, -kPio8Hi, x);
+  r = fmad(kd, -kPio8Lo, r);
+  const double z = r * r;
+  double ps = fmad(z, kStepS2, kStepS1);
+  ps = fmad(ps, z, kStepS0);
+  const double sr = fmad(r * z, ps, r);
+  double pc = fmad(z, kStepC2, kStepC1);
+  pc = fmad(pc, z, kStepC0);
+  const double cr = fmad(pc, z, 1.0);
+  *c_out = fmad(cos16[q], cr, -(sin16[q] * sr));
+  *s_out = fmad(sin16[q], cr, cos16[q] * sr);
+}
+
 }  // namespace uwb

@@ -54,3 +54,30 @@ def test_cxx_optimise_matches_reference_optimiser():
     assert d["lbfgs_iterations"] == ref["lbfgs_iterations"]
     assert ref["rel_dobjective"] < 1e-9
     assert ref["max_abs_dx_db"] < 1e-6
+
+
+@pytest.mark.gpu
+def test_cxx_optimise_segmented_matches_reference_optimiser():
+    """Config 5 exactly as BASELINE defines it: SEGMENTED mode (55 variables
+    for the 589-ch plan, link_optimizer.hpp:68-102 / test_optimizer.cpp:127-133),
+    bounds [-5, 5] dBm, fd step 1e-3 dB, 2 L-BFGS-B iterations at N_R = 24.
+    Every cost call (value, 55-wide forward-difference batches, backtracks)
+    runs on the device through the C++ drop-in; the reference CPU optimiser
+    runs the same problem.  Same iteration count, objective within 1e-9,
+    iterate within 1e-6 dB."""
+    import json
+
+    if not os.path.exists(OPT):
+        pytest.skip("oracle/_ref/optimise_b200 not built (needs /root/reference at build time)")
+    r = subprocess.run([OPT, "--iters", "2", "--n-r", "24", "--density", "0.95", "--uniform", "0",
+                        "--reference-iters", "2", "--devices", "1"],
+                       capture_output=True, text=True, timeout=1800)
+    assert r.returncode == 0, r.stdout + r.stderr
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    print(d)
+    assert "segmented" in d["config"]
+    ref = d["reference"]
+    assert d["lbfgs_iterations"] == ref["lbfgs_iterations"] == 2
+    assert d["cost_evals"] >= 1 + 2 * 56  # value + two 55-wide gradients at least
+    assert ref["rel_dobjective"] < 1e-9
+    assert ref["max_abs_dx_db"] < 1e-6

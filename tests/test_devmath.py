@@ -1,7 +1,12 @@
-"""CPU: the integrand's FP64 transcendentals (csrc/uwb_devmath.cuh are
-__host__ __device__) against long-double libm.  The device versions in
-nli_kernel.cu use the same coefficients; the GPU parity tests cover them end
-to end."""
+"""CPU: the integrand's FP64 transcendentals against long-double libm.
+
+csrc/uwb_devmath.cuh holds __host__ __device__ restatements of the device
+code: the ulp-accurate kernels of the row setup (exp2_16, sincos_tab16) and
+the SHORTER step kernels the hot loop actually runs at UWB_FAST_POLY=2
+(step_exp2_16, step_sincos_tab16: 2^x quartic, sin degree 7, cos degree 6),
+whose coefficients nli_kernel.cu's __constant__ banks are initialised from
+(checked below).  Their documented error bounds are asserted here; the GPU
+parity tests cover the kernels end to end."""
 import ctypes
 import os
 import subprocess
@@ -29,6 +34,11 @@ void sincos16_v(const double* x, double* c, double* s, long n) { for (long i = 0
 double err_sincos16(const double* x, long n) { long double m = 0; for (long i = 0; i < n; ++i) {
   double c, s; uwb::sincos_tab16(x[i], C16, S16, &c, &s); long double ec = fabsl(c - cosl((long double)x[i])), es = fabsl(s - sinl((long double)x[i]));
   if (ec > m) m = ec; if (es > m) m = es; } return (double)m; }
+double err_step_exp2_16(const double* x, long n) { long double m = 0; for (long i = 0; i < n; ++i) {
+  long double r = exp2l((long double)x[i] / 16); long double e = fabsl((uwb::step_exp2_16(x[i], T16) - r) / r); if (e > m) m = e; } return (double)m; }
+double err_step_sincos16(const double* x, long n, int which) { long double m = 0; for (long i = 0; i < n; ++i) {
+  double c, s; uwb::step_sincos_tab16(x[i], C16, S16, &c, &s); long double ec = fabsl(c - cosl((long double)x[i])), es = fabsl(s - sinl((long double)x[i]));
+  long double e = which == 0 ? ec : es; if (e > m) m = e; } return (double)m; }
 double err_sincos(const double* x, long n) { long double m = 0; for (long i = 0; i < n; ++i) {
   double c, s; uwb::sincos_rd(x[i], &c, &s); long double ec = fabsl(c - cosl((long double)x[i])), es = fabsl(s - sinl((long double)x[i]));
   if (ec > m) m = ec; if (es > m) m = es; } return (double)m; }
@@ -49,6 +59,8 @@ def lib(tmp_path_factory):
     L.err_exp2_16.restype = ctypes.c_double
     L.err_sincos.restype = ctypes.c_double
     L.err_sincos16.restype = ctypes.c_double
+    L.err_step_exp2_16.restype = ctypes.c_double
+    L.err_step_sincos16.restype = ctypes.c_double
     return L
 
 
@@ -91,3 +103,34 @@ def test_sincos_table16_exact_zero_and_quadrants(lib):
     lib.sincos16_v(_p(x), _p(c), _p(s), 4)
     assert c[0] == 1.0 and s[0] == 0.0
     assert np.allclose(c, np.cos(x), atol=3e-16) and np.allclose(s, np.sin(x), atol=3e-16)
+
+
+# ---------------------------------------------------------------- step kernels (hot loop)
+def test_step_exp2_16_error_bound(lib):
+    """The hot loop's 2^(x/16) (quartic on |r| <= 1/2): relative error <= 5e-12
+    (DESIGN.md §3.1), over the integrand's argument range."""
+    x = np.random.default_rng(4).uniform(-40 * 16, 4 * 16, 400000)
+    e = lib.err_step_exp2_16(_p(x), len(x))
+    assert 1e-13 < e < 5.5e-12  # a real truncation error, within the documented bound
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e3, 1e6, 3e7])
+def test_step_sincos_error_bounds(lib, scale):
+    """The hot loop's sincos at UWB_FAST_POLY=2: the kernels are cos degree 6
+    (1.7e-12) and sin degree 7 (3.7e-14) on |r| <= pi/16; the angle addition
+    with the (cos, sin)(k pi/8) table mixes them, so cos x and sin x each stay
+    within 1.75e-12 absolute -- and no better than ~1e-13 (a real truncation)."""
+    x = np.random.default_rng(5).uniform(-scale, scale, 300000)
+    ec = lib.err_step_sincos16(_p(x), len(x), 0)
+    es = lib.err_step_sincos16(_p(x), len(x), 1)
+    assert 1e-13 < ec < 1.75e-12 and 1e-13 < es < 1.75e-12, (ec, es)
+
+
+def test_step_kernel_coefficients_are_the_device_ones():
+    """nli_kernel.cu's __constant__ banks are initialised from the header's
+    kStep* constants (the ones the host restatements above use)."""
+    src = open(os.path.join(ROOT, "paper_2401_18022_b200", "csrc", "nli_kernel.cu")).read()
+    assert "c_e4f[4] = {kStepE0, kStepE1, kStepE2, kStepE3}" in src
+    assert "c_s3f[3] = {kStepS0, kStepS1, kStepS2}" in src
+    assert "c_c3f[3] = {kStepC0, kStepC1, kStepC2}" in src
+    assert "#define UWB_FAST_POLY 2" in src
