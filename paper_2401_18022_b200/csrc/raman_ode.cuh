@@ -9,8 +9,14 @@
 
 namespace uwb {
 
-constexpr int kMaxOdeChannels = 2560;  // 512 threads x 5 channels per thread
-constexpr int kMaxRamanSegments = 4;  // linear pieces of the gain table in d = |j - i|
+// Channels the device ODE takes: 32 warps x 7 channels per thread.  Combs
+// whose prefix arrays fit the opt-in shared memory run from shared memory,
+// larger ones from an L1/L2-resident global work buffer (OdeParams::gwork).
+constexpr int kMaxOdeChannels = 32 * 32 * 7;
+// Linear pieces of the gain table in d = |j - i| (TabulatedProfile rows - 1
+// plus zero fill between pieces); edges = pieces + 1.
+constexpr int kMaxRamanSegments = 64;
+constexpr int kMaxRamanEdges = kMaxRamanSegments + 1;
 
 struct OdeParams {
   int n;                 // channels
@@ -19,11 +25,17 @@ struct OdeParams {
   double* coef_a;        // [n] f_i aeff_ref / aeff_i          (filled on device)
   double* coef_u;        // [n] P_i / f_i                      (filled on device)
   double* coef_v;        // [n] aeff_ref P_i / aeff_i          (filled on device)
-  int n_seg;             // gain table as G = a + b d on d in [dlo, dhi]
-  int seg_dlo[kMaxRamanSegments];
-  int seg_dhi[kMaxRamanSegments];
-  double seg_a[kMaxRamanSegments];
-  double seg_b[kMaxRamanSegments];
+  // Gain table G(d), d = |j - i|, as contiguous pieces a_g + b_g d on
+  // [edge[g], edge[g + 1]), written in summation-by-parts form: the window
+  // sums of piece g enter through their two edges, so edge k carries the
+  // jumps da_k = a_k - a_{k-1}, db_k = b_k - b_{k-1} (a_{-1} = a_{n_seg} = 0),
+  // folded into the per-edge gather coefficients cu_k = da_k + db_k E_k,
+  // cv_k = da_k + db_k (E_k - 1) (raman_ode.cu rhs).
+  int n_seg;
+  int edge[kMaxRamanEdges];
+  double cu[kMaxRamanEdges];
+  double cv[kMaxRamanEdges];
+  double db[kMaxRamanEdges];
   int steps;             // distance-grid steps (midpoints)
   int col_stride;        // row stride of log2rho / log_rho (>= steps)
   int lane_k;            // > 0: log2rho in the integrand's lane order lane_pos(m, lane_k)
@@ -36,19 +48,27 @@ struct OdeParams {
   double* rho_end;       // [n] out
   int* status;           // out: 0 ok, 1 non-positive rho, 2 step budget, 3 step underflow
   long long* rhs_evals;  // out (may be null)
+  double2* gwork;        // global prefix-array fallback, ode_gwork_double2(n) entries
+  long long* prof;       // instrumented build only (UWB_ODE_PROF): phase cycle sums
 };
 
-// Gain table (x, y) -> d-segments for channel spacing `spacing` (host).
-// Returns 0, or -1 if the table does not fit kMaxRamanSegments.
+// Gain table (x, y) -> pieces and edges for channel spacing `spacing` (host).
+// Returns 0, or -1 if the table needs more than kMaxRamanSegments pieces.
 int raman_segments(const double* x, const double* y, int rn, double spacing, int n_ch,
                    OdeParams* P);
 
+// double2 entries of the global work buffer launch_raman_ode may use (callers
+// allocate it once and pass it in OdeParams::gwork).
+size_t ode_gwork_double2(int n);
+
 // Fills the per-channel coupling factors from the launch PSD and runs the
-// one-CTA ODE kernel.  Returns kernel launches issued, or < 0 on failure.
-// max_ept > 0 overrides the channels-per-thread choice (5 keeps the 589-ch
-// solve on 128 threads x <= 255 registers: it then fits on an SM beside one
-// integrand CTA, for overlapped batches).
+// one-CTA ODE kernel.  Returns kernel launches issued, or < 0 on failure
+// (-1: n out of range, -2: launch error).
 int launch_raman_ode(OdeParams P, const double* freq, const double* psd, double bch,
-                     const double* aeff, double aeff_ref, cudaStream_t st, int max_ept = 0);
+                     const double* aeff, double aeff_ref, cudaStream_t st);
+
+// The (warps, channels per thread) split launch_raman_ode picks for n
+// channels (UWB_ODE_SPLIT="W,EPT" overrides it for experiments).
+void ode_split(int n, int* warps, int* ept);
 
 }  // namespace uwb

@@ -373,7 +373,7 @@ void uwb_ctx_destroy(uwb_ctx* c) {
                   &c->wlast, &c->probe_nu, &c->probe_gamma, &c->hl2, &c->rowsum, &c->counter,
                   &c->n_eval, &c->probe_g, &c->probe_quad, &c->chan_probe0, &c->eta, &c->nli_psd,
                   &c->nli_power, &c->quad, &c->skipped, &c->batch_psd, &c->batch_report, &c->batch_ode, &c->alpha, &c->aeff, &c->raman_x,
-                  &c->raman_y, &c->nf_db, &c->guard, &c->rho_end, &c->ode_work, &c->report,
+                  &c->raman_y, &c->nf_db, &c->guard, &c->rho_end, &c->ode_work, &c->ode_gwork, &c->report,
                   &c->mid, &c->edge})
     b->release();
   if (c->pinned) cudaFreeHost(c->pinned);

@@ -72,7 +72,7 @@ struct uwb_ctx {
   };
   BatchState* batch = nullptr;
   // link evaluation state (raman ODE + assembly)
-  uwb::DBuf alpha, aeff, raman_x, raman_y, nf_db, guard, rho_end, ode_work, report, mid, edge;
+  uwb::DBuf alpha, aeff, raman_x, raman_y, nf_db, guard, rho_end, ode_work, ode_gwork, report, mid, edge;
   std::vector<int> subset;
   // stats of the last call
   unsigned long long h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of the last call

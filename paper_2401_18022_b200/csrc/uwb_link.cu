@@ -353,7 +353,12 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   O.alpha = d_alpha;
   if (O.raman && raman_segments(fb->raman_x, fb->raman_y, fb->raman_n, g->spacing, n, &O))
     return fail(UWB_CONFIG_ERROR, "raman gain table has too many linear pieces");
-  if (n > kMaxOdeChannels) return fail(UWB_CONFIG_ERROR, "uwb: at most 2560 channels");
+  if (n > kMaxOdeChannels) return fail(UWB_CONFIG_ERROR, "uwb: at most 7168 channels");
+  // global fallback for the ODE's running-sum arrays (combs too wide for
+  // shared memory), two halves for the overlapped batch's two ODEs in flight
+  const size_t gw = ode_gwork_double2(n);
+  O.gwork = c->ode_gwork.get<double2>(2 * gw);
+  if (!O.gwork) return fail(UWB_CUDA_ERROR, "device allocation failed");
   // ode_work: coef a|u|v [3n] | rho_end [n] | status, rhs [2] | band [n ints] | link tmp [3n]
   double* w = c->ode_work.get<double>(3 * static_cast<size_t>(n) + n + 2 + n + 3 * n + 8);
   if (!w) return fail(UWB_CUDA_ERROR, "device allocation failed");
@@ -563,6 +568,7 @@ int uwb_evaluate_link_many(uwb_ctx* c, int n_eval, const double* psd_host, doubl
     Ob[1].coef_a = wb + tab + n;
     Ob[1].coef_u = wb + tab + 2 * n;
     Ob[1].coef_v = wb + tab + 3 * n;
+    Ob[1].gwork = pr->O.gwork + ode_gwork_double2(static_cast<int>(n));
     cudaEventRecord(B.ev_start, st);
     cudaStreamWaitEvent(B.s_ode, B.ev_start, 0);  // uploads / status reset first
     for (int e = 0; e < n_eval; ++e) {
@@ -571,7 +577,7 @@ int uwb_evaluate_link_many(uwb_ctx* c, int n_eval, const double* psd_host, doubl
       Pb[b].psd = Fb[b].psd = Lb[b].psd = psd_e;
       if (e >= 2) cudaStreamWaitEvent(B.s_ode, B.ev_nli[b], 0);  // eval e-2 done with buffer b
       const int lo = launch_raman_ode(Ob[b], pr->P.freq, psd_e, pr->P.bch, pr->d_aeff, pr->aeff_ref,
-                                      B.s_ode, /*max_ept=*/5);
+                                      B.s_ode);
       if (lo < 0) return fail(UWB_CUDA_ERROR, "raman ODE launch failed");
       cudaEventRecord(B.ev_ode[b], B.s_ode);
       cudaStreamWaitEvent(st, B.ev_ode[b], 0);
@@ -726,7 +732,7 @@ int uwb_power_evolution(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre
   const double* d_mid = up(c, c->mid, mid, steps);
   if (link->include_raman && (fibre->raman_n < 2 || !fibre->raman_x || !fibre->raman_y))
     return fail(UWB_CONFIG_ERROR, "raman gain: table needs at least two (x, y) rows");
-  if (n > kMaxOdeChannels) return fail(UWB_CONFIG_ERROR, "uwb: at most 2560 channels");
+  if (n > kMaxOdeChannels) return fail(UWB_CONFIG_ERROR, "uwb: at most 7168 channels");
   // ode_work: log2 [n*steps] | ln [n*steps] | rho_end [n] | status, rhs [2] | coef a|u|v [3n]
   const size_t ns = static_cast<size_t>(n) * steps;
   double* w = c->ode_work.get<double>(2 * ns + n + 2 + 3 * n);
@@ -758,6 +764,8 @@ int uwb_power_evolution(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre
   O.rho_end = d_re;
   O.status = d_status;
   O.rhs_evals = d_rhs;
+  O.gwork = c->ode_gwork.get<double2>(ode_gwork_double2(n));
+  if (!O.gwork) return fail(UWB_CUDA_ERROR, "device allocation failed");
   cudaMemsetAsync(d_status, 0, sizeof(int), st);
   const int lo = launch_raman_ode(O, d_freq, d_psd, grid->bch, d_aeff, fibre->raman_aeff_ref, st);
   if (lo < 0) return fail(UWB_CUDA_ERROR, "raman ODE launch failed");
