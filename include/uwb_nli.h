@@ -147,6 +147,33 @@ int uwb_device_count(int* n);
 /* Context: binds one CUDA device (0-based index within CUDA_VISIBLE_DEVICES). */
 int uwb_ctx_create(int device, uwb_ctx** out);
 void uwb_ctx_destroy(uwb_ctx* ctx);
+
+/* Multi-GPU context = the reference's worker pool (GnSolverConfig::workers,
+ * all_channels_nli's parallel_for_batches, gn_integral.hpp:348 ->
+ * parallel.hpp:21-47) with GPUs as the workers.  devices[0..n_devices) are
+ * CUDA device indices (repeats allowed, e.g. several contexts on one GPU);
+ * devices[0] leads.  Every entry point accepts the returned context:
+ *  - uwb_all_channels_nli, uwb_evaluate_link, uwb_evaluate_link_prepare /
+ *    _resident split the channels into contiguous ranges balanced by the
+ *    per-channel work the previous NLI measured; each GPU runs the Raman ODE
+ *    and its range's NLI; eta slices are gathered on the lead
+ *    (cudaMemcpyPeerAsync over NVLink), which assembles the report.
+ *    _resident's psd_dev / report_dev / stream live on the lead device;
+ *  - uwb_evaluate_link_many deals whole evaluations to the GPUs;
+ *  - nli_psd_at, channel_nli, power_evolution and the closed form run on the
+ *    lead;
+ *  - uwb_set_channel_subset and the split _resident_noise / _report /
+ *    uwb_link_eta_buffer stages are single-device: ConfigError.
+ * Results are bit-identical to one device for any device list. */
+int uwb_ctx_create_multi(const int* devices, int n_devices, uwb_ctx** out);
+/* Devices behind a context (1 for uwb_ctx_create). */
+int uwb_ctx_width(uwb_ctx* ctx, int* n);
+/* |K|^2 evaluations per channel of the last NLI ([n_ch]; the multi-GPU
+ * split's cost model, measured on the device). */
+int uwb_last_channel_work(uwb_ctx* ctx, int n_ch, double* work);
+/* Per device of the last split evaluation: integrand and ODE device time
+ * (ms) and the first channel of its range ([n] each, any may be NULL). */
+int uwb_last_partition_stats(uwb_ctx* ctx, int n, double* nli_ms, double* ode_ms, int* first_ch);
 int uwb_device_info(uwb_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor);
 
 /* Restrict all_channels_nli / evaluate_link to a subset of channels (multi-GPU

@@ -25,8 +25,10 @@
 // and linking libuwbnli.so.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstddef>
+#include <cstdlib>
 #include <cstdint>
 #include <memory>
 #include <mutex>
@@ -60,6 +62,11 @@ inline void check(int rc) {
 class Engine {
  public:
   explicit Engine(int device = 0) { check(uwb_ctx_create(device, &ctx_)); }
+  // Multi-GPU context over `devices` (uwb_ctx_create_multi): the channels of
+  // interest are split over the GPUs, bit-identical to one GPU.
+  explicit Engine(const std::vector<int>& devices) {
+    check(uwb_ctx_create_multi(devices.data(), static_cast<int>(devices.size()), &ctx_));
+  }
   ~Engine() { uwb_ctx_destroy(ctx_); }
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -69,10 +76,42 @@ class Engine {
   uwb_ctx* ctx_ = nullptr;
 };
 
-inline Engine& engine() {
-  thread_local std::unique_ptr<Engine> e;
-  if (!e) e = std::make_unique<Engine>(0);
-  return *e;
+// The GPUs the drop-in may use: UWB_DEVICES="0,2,..." or every visible one.
+inline std::vector<int> visible_devices() {
+  std::vector<int> d;
+  if (const char* e = std::getenv("UWB_DEVICES")) {
+    const std::string s(e);
+    std::size_t p = 0;
+    while (p < s.size()) {
+      const std::size_t q = s.find(',', p);
+      d.push_back(std::stoi(s.substr(p, q == std::string::npos ? std::string::npos : q - p)));
+      if (q == std::string::npos) break;
+      p = q + 1;
+    }
+    if (!d.empty()) return d;
+  }
+  int n = 0;
+  check(uwb_device_count(&n));
+  for (int k = 0; k < n; ++k) d.push_back(k);
+  return d;
+}
+
+// The engine for the reference's worker count (GnSolverConfig::workers,
+// gn_integral.hpp:22): the workers of parallel_for_batches (parallel.hpp:
+// 12-16, 0 = every hardware thread) are GPUs here -- 0 = every GPU of
+// visible_devices(), k = the first min(k, n) of them.  One context per
+// calling thread (the reference is reentrant) and per width.
+inline Engine& engine(int workers = 1) {
+  thread_local std::vector<std::unique_ptr<Engine>> cache;
+  const std::vector<int> all = visible_devices();
+  int w = workers <= 0 ? static_cast<int>(all.size()) : std::min<int>(workers, static_cast<int>(all.size()));
+  w = std::max(1, w);
+  if (cache.size() < static_cast<std::size_t>(w) + 1) cache.resize(w + 1);
+  if (!cache[w]) {
+    if (w == 1) cache[w] = std::make_unique<Engine>(all.empty() ? 0 : all[0]);
+    else cache[w] = std::make_unique<Engine>(std::vector<int>(all.begin(), all.begin() + w));
+  }
+  return *cache[w];
 }
 
 namespace detail {
@@ -196,8 +235,8 @@ inline FibreSamples fibre_samples(const FibreSpec& fibre, const ChannelGrid& gri
   return out;
 }
 
-// all_channels_nli (gn_integral.hpp:334-363).  cfg.workers has no meaning on
-// the device; results are identical for any value (and any GPU count).
+// all_channels_nli (gn_integral.hpp:334-363).  cfg.workers picks the GPUs
+// (engine(workers): 0 = all); results are identical for any value.
 [[nodiscard]] inline NliResult all_channels_nli(const ChannelGrid& grid,
                                                 const std::vector<PowerEvolution>& spans,
                                                 const BetaCoefficients& betas,
@@ -226,8 +265,8 @@ inline FibreSamples fibre_samples(const FibreSpec& fibre, const ChannelGrid& gri
   o.nli_power = r.nli_power.data();
   o.quadrant = quad.data();
   o.skipped = r.skipped.data();
-  check(uwb_all_channels_nli(engine().get(), &g, static_cast<int>(sv.size()), sv.data(), beta,
-                             gamma.data(), &c, &o));
+  check(uwb_all_channels_nli(engine(cfg.workers).get(), &g, static_cast<int>(sv.size()), sv.data(),
+                             beta, gamma.data(), &c, &o));
   for (std::size_t ch = 0; ch < n; ++ch)
     for (int q = 0; q < 4; ++q) r.quadrant[ch][q] = quad[4 * ch + q];
   r.elapsed_seconds = o.elapsed_seconds;
@@ -298,7 +337,7 @@ inline FibreSamples fibre_samples(const FibreSpec& fibre, const ChannelGrid& gri
   o.rho_end = rho_end.data();
   o.band_power_dbm = bpow.data();
   o.band_capacity = bcap.data();
-  check(uwb_evaluate_link(engine().get(), &g, &fs.f, &lk, &c, &o));
+  check(uwb_evaluate_link(engine(gn.workers).get(), &g, &fs.f, &lk, &c, &o));
   LinkReport rep;
   rep.channels.resize(n);
   for (std::size_t i = 0; i < n; ++i) {
@@ -342,7 +381,7 @@ inline FibreSamples fibre_samples(const FibreSpec& fibre, const ChannelGrid& gri
   uwb_link_report o{};
   o.eta = out.eta.data();
   o.rho_end = out.rho_end.data();
-  check(uwb_evaluate_link(engine().get(), &g, &fs.f, &lk, &c, &o));
+  check(uwb_evaluate_link(engine(gn.workers).get(), &g, &fs.f, &lk, &c, &o));
   return out;
 }
 

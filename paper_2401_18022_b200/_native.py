@@ -95,6 +95,10 @@ SIGNATURES = {
     "uwb_abi_version": (C.c_int, []),
     "uwb_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "uwb_ctx_destroy": (None, [C.c_void_p]),
+    "uwb_ctx_create_multi": (C.c_int, [IP, C.c_int, C.POINTER(C.c_void_p)]),
+    "uwb_ctx_width": (C.c_int, [C.c_void_p, IP]),
+    "uwb_last_channel_work": (C.c_int, [C.c_void_p, C.c_int, DP]),
+    "uwb_last_partition_stats": (C.c_int, [C.c_void_p, C.c_int, DP, DP, IP]),
     "uwb_device_info": (C.c_int, [C.c_void_p, IP, IP, IP]),
     "uwb_set_channel_subset": (C.c_int, [C.c_void_p, C.c_int, IP]),
     "uwb_all_channels_nli": (C.c_int, [C.c_void_p, C.POINTER(Grid), C.c_int, C.POINTER(Span), DP,

@@ -19,7 +19,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "libuwbnli.so")
 SOURCES = ["nli_kernel.cu", "raman_ode.cu", "uwb_capi.cu", "uwb_link.cu", "uwb_model.cu",
-           "uwb_cfm.cu"]
+           "uwb_cfm.cu", "uwb_multi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
          "-Xptxas", "-warn-spills"]

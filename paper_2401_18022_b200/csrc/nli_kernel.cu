@@ -782,6 +782,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
       P.rowsum[row] = acc * du1 * S.du2;
       atomicAdd(P.n_eval, static_cast<unsigned long long>(n_eval));
       atomicAdd(P.n_active, static_cast<unsigned long long>(n_act_row));
+      if (P.probe_work) atomicAdd(P.probe_work + probe, static_cast<unsigned long long>(n_eval));
     }
     __syncwarp();
 
@@ -1040,6 +1041,7 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
   int launches = 0;
   cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), stream);
   cudaMemsetAsync(p.n_eval, 0, 2 * sizeof(unsigned long long), stream);  // n_eval, n_active
+  if (p.probe_work) cudaMemsetAsync(p.probe_work, 0, p.n_probes * sizeof(unsigned long long), stream);
   probe_halflog_kernel<<<p.n_probes, 128, 0, stream>>>(p);
   ++launches;
   if (ev_k0) cudaEventRecord(ev_k0, stream);

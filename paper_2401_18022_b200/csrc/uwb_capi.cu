@@ -17,6 +17,7 @@
 #include "uwb_capi_internal.cuh"
 #include "uwb_ctx.cuh"
 #include "uwb_devmath.cuh"
+#include "uwb_multi.cuh"
 
 namespace {
 
@@ -220,6 +221,7 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
   P.counter = c->counter.get<unsigned int>(1);
   P.n_eval = c->n_eval.get<unsigned long long>(2);
   P.n_active = P.n_eval + 1;
+  P.probe_work = c->probe_work.get<unsigned long long>(std::max(np, 1));
   F.probe_gamma = d_g;
   F.probe_g = c->probe_g.get<double>(std::max(np, 1));
   F.probe_quad = c->probe_quad.get<double>(4 * std::max(np, 1));
@@ -230,6 +232,10 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
     xfer(c, d_nu, nu.data(), np * sizeof(double), cudaMemcpyHostToDevice, st);
     xfer(c, d_g, gam.data(), np * sizeof(double), cudaMemcpyHostToDevice, st);
   }
+  c->last_n_probes = np;
+  c->last_probes_per_chan = cfg->simpson ? 3 : 1;
+  if (chan_probe0) c->last_chan_probe0 = *chan_probe0;
+  else c->last_chan_probe0.clear();
   if (chan_probe0) {
     const int n = P.n_ch;
     int* d_cp = c->chan_probe0.get<int>(n);
@@ -369,8 +375,13 @@ void uwb_ctx_destroy(uwb_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   release_link_state(c);
+  for (uwb_ctx* s : c->subs) uwb_ctx_destroy(s);
+  for (uwb_ctx* s : c->bsubs) uwb_ctx_destroy(s);
+  c->subs.clear();
+  c->bsubs.clear();
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
   for (DBuf* b : {&c->freq, &c->psd, &c->gamma, &c->log2rho, &c->zedge, &c->zstart, &c->zmid, &c->width,
-                  &c->wlast, &c->probe_nu, &c->probe_gamma, &c->hl2, &c->rowsum, &c->counter,
+                  &c->wlast, &c->probe_nu, &c->probe_chan, &c->probe_work, &c->probe_gamma, &c->hl2, &c->rowsum, &c->counter,
                   &c->n_eval, &c->probe_g, &c->probe_quad, &c->chan_probe0, &c->eta, &c->nli_psd,
                   &c->nli_power, &c->quad, &c->skipped, &c->batch_psd, &c->batch_report, &c->batch_ode, &c->alpha, &c->aeff, &c->raman_x,
                   &c->raman_y, &c->nf_db, &c->guard, &c->rho_end, &c->ode_work, &c->ode_gwork, &c->report,
@@ -393,6 +404,7 @@ void uwb_ctx_destroy(uwb_ctx* c) {
 
 int uwb_device_info(uwb_ctx* c, int* sm_count, int* cc_major, int* cc_minor) {
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  if (c->multi()) return uwb_device_info(c->subs[0], sm_count, cc_major, cc_minor);
   if (sm_count) *sm_count = c->sm_count;
   if (cc_major) *cc_major = c->cc_major;
   if (cc_minor) *cc_minor = c->cc_minor;
@@ -401,6 +413,7 @@ int uwb_device_info(uwb_ctx* c, int* sm_count, int* cc_major, int* cc_minor) {
 
 int uwb_set_channel_subset(uwb_ctx* c, int n, const int* channels) {
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  if (c->multi()) return set_err(UWB_CONFIG_ERROR, "a multi-GPU context partitions the channels itself");
   c->subset.assign(channels, channels + std::max(n, 0));
   if (n > 0 && !channels) return set_err(UWB_CONFIG_ERROR, "null channel list");
   return UWB_OK;
@@ -410,6 +423,7 @@ int uwb_all_channels_nli(uwb_ctx* c, const uwb_grid* grid, int n_spans, const uw
                          const double beta[3], const double* gamma, const uwb_nli_cfg* cfg,
                          uwb_nli_result* out) {
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  if (c->multi()) return multi_all_channels_nli(c, grid, n_spans, spans, beta, gamma, cfg, out);
   cudaSetDevice(c->device);
   release_link_state(c);  // shares buffers with the prepared evaluation
   reset_xfer(c);
@@ -460,6 +474,8 @@ int uwb_nli_psd_at(uwb_ctx* c, const uwb_grid* grid, int n_spans, const uwb_span
                    const double beta[3], const uwb_nli_cfg* cfg, int n_probe, const double* nu,
                    const double* gamma, double* out, double* quadrant4) {
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  if (c->multi())
+    return uwb_nli_psd_at(c->subs[0], grid, n_spans, spans, beta, cfg, n_probe, nu, gamma, out, quadrant4);
   cudaSetDevice(c->device);
   release_link_state(c);
   reset_xfer(c);
@@ -501,11 +517,30 @@ int uwb_channel_nli(uwb_ctx* c, const uwb_grid* grid, int n_spans, const uwb_spa
   return UWB_OK;
 }
 
-int uwb_last_launch_count(uwb_ctx* c) { return c ? c->last_launches : 0; }
+int uwb_last_launch_count(uwb_ctx* c) {
+  if (!c) return 0;
+  return c->multi() ? c->subs[0]->last_launches : c->last_launches;
+}
 
 int uwb_last_nli_stats(uwb_ctx* c, double* kernel_ms, double* inner_steps,
                        double* evaluated_points) {
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  if (c->multi()) {  // max kernel time over devices, summed work
+    double km = 0.0, st = 0.0, pt = 0.0;
+    for (uwb_ctx* s : c->subs) {
+      double a = 0.0, b = 0.0, d = 0.0;
+      uwb_last_nli_stats(s, &a, &b, &d);
+      km = std::max(km, a);
+      st += b;
+      pt += d;
+    }
+    c->last_active = 0.0;
+    for (uwb_ctx* s : c->subs) c->last_active += s->last_active;
+    if (kernel_ms) *kernel_ms = km;
+    if (inner_steps) *inner_steps = st;
+    if (evaluated_points) *evaluated_points = pt;
+    return UWB_OK;
+  }
   // Resolved lazily from the events/counter of the last integrand launch (the
   // caller has synchronised), so the resident path pays nothing per call.
   if (c->nli_events_valid) {
@@ -534,6 +569,7 @@ int uwb_last_nli_active(uwb_ctx* c, double* active_points) {
 
 int uwb_last_transfer_bytes(uwb_ctx* c, unsigned long long* h2d, unsigned long long* d2h) {
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  if (c->multi()) return uwb_last_transfer_bytes(c->subs[0], h2d, d2h);
   if (h2d) *h2d = c->h2d_bytes;
   if (d2h) *d2h = c->d2h_bytes;
   return UWB_OK;
@@ -541,6 +577,8 @@ int uwb_last_transfer_bytes(uwb_ctx* c, unsigned long long* h2d, unsigned long l
 
 int uwb_set_precision(uwb_ctx* c, int mode) {
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  for (uwb_ctx* s : c->subs) uwb_set_precision(s, mode);
+  for (uwb_ctx* s : c->bsubs) uwb_set_precision(s, mode);
   if (mode != UWB_PRECISION_FP64 && mode != UWB_PRECISION_MIXED)
     return set_err(UWB_CONFIG_ERROR, "uwb_set_precision: unknown mode");
   c->precision = mode;
@@ -549,6 +587,8 @@ int uwb_set_precision(uwb_ctx* c, int mode) {
 
 int uwb_set_ode_stepping(uwb_ctx* c, int mode) {
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  for (uwb_ctx* s : c->subs) uwb_set_ode_stepping(s, mode);
+  for (uwb_ctx* s : c->bsubs) uwb_set_ode_stepping(s, mode);
   if (mode != UWB_ODE_RESTART && mode != UWB_ODE_CONTINUOUS)
     return set_err(UWB_CONFIG_ERROR, "uwb_set_ode_stepping: unknown mode");
   c->ode_continuous = mode == UWB_ODE_CONTINUOUS ? 1 : 0;
@@ -557,6 +597,7 @@ int uwb_set_ode_stepping(uwb_ctx* c, int mode) {
 
 int uwb_fp64_peak(uwb_ctx* c, double* tflops) {
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
+  if (c->multi()) return uwb_fp64_peak(c->subs[0], tflops);
   cudaSetDevice(c->device);
   const double t = fp64_fma_peak_tflops(c->sm_count, c->stream);
   if (!(t > 0)) return set_err(UWB_CUDA_ERROR, "fp64 microbenchmark failed");

@@ -156,6 +156,7 @@ extern "C" int uwb_cfm_all_channels_nli(uwb_ctx* c, const uwb_grid* grid, int n_
                                         const uwb_span* spans, const double beta[3],
                                         const double* gamma, uwb_nli_result* out) {
   if (!c) return fail(UWB_CONFIG_ERROR, "null context");
+  if (c->multi()) return uwb_cfm_all_channels_nli(c->subs[0], grid, n_spans, spans, beta, gamma, out);
   cudaSetDevice(c->device);
   reset_xfer(c);
   int rc = validate_grid(grid);

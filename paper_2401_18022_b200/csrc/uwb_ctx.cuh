@@ -59,6 +59,7 @@ struct uwb_ctx {
   // spans
   uwb::DBuf log2rho, zedge, zstart, zmid, width, wlast;
   // probes + work
+  uwb::DBuf probe_work;  // per-probe |K|^2 evaluations of the last NLI
   uwb::DBuf probe_nu, probe_chan, probe_gamma, hl2, rowsum, counter, n_eval, probe_g, probe_quad, chan_probe0;
   // per-channel results
   uwb::DBuf eta, nli_psd, nli_power, quad, skipped;
@@ -86,7 +87,21 @@ struct uwb_ctx {
   // pinned host staging for small transfers
   void* pinned = nullptr;
   size_t pinned_cap = 0;
+  // probes of the last NLI: first probe of each channel (-1: none) and
+  // probes per channel (3 with Simpson), for uwb_last_channel_work
+  std::vector<int> last_chan_probe0;
+  int last_probes_per_chan = 1;
+  int last_n_probes = 0;
   // prepared link problem (uwb_evaluate_link_prepare)
   struct Prepared;
   Prepared* prep = nullptr;
+  // Multi-device context (uwb_ctx_create_multi): the reference's channel-
+  // parallel worker pool (parallel_for_batches, parallel.hpp:21-47) as a
+  // partition of the channels over GPUs.  subs[0] is the lead.
+  std::vector<uwb_ctx*> subs;   // channel-split evaluation, one per device entry
+  std::vector<uwb_ctx*> bsubs;  // whole evaluations of a batch (uwb_evaluate_link_many)
+  std::vector<double> chan_cost;  // per-channel work of the last NLI (balances the next split)
+  std::vector<int> part_lo;       // channel ranges [part_lo[d], part_lo[d+1]) of the last split
+  cudaEvent_t ev_done = nullptr;  // this context's noise stage is complete (multi gather)
+  bool multi() const { return !subs.empty(); }
 };

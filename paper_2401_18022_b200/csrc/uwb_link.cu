@@ -18,6 +18,8 @@
 #include "uwb_capi_internal.cuh"
 #include "uwb_ctx.cuh"
 #include "uwb_devmath.cuh"
+#include "uwb_link.cuh"
+#include "uwb_multi.cuh"
 
 namespace uwb {
 
@@ -25,23 +27,7 @@ namespace {
 
 constexpr double kPlanck = 6.62607015e-34;  // units.hpp:10
 
-struct LinkDev {
-  int n;
-  const double* freq;
-  const double* psd;
-  const uint8_t* guard;
-  double bch;
-  const double* eta;
-  const double* rho_end;
-  const double* nf_db;
-  const int* band;
-  int n_bands;
-  int span_count;
-  int use_snr_trx;
-  double snr_trx;
-  double* out;  // [4n] eta | p_ase | snr_db | capacity, then [3] totals, then [2*n_bands]
-  double* tmp;  // [3n] per-channel p, capacity, log2(1+snr) for the ordered sums
-};
+
 
 // Per-channel part of assemble_link_report (link_optimizer.hpp:206-224).
 __global__ void link_channels_kernel(LinkDev L) {
@@ -87,7 +73,6 @@ __global__ void link_channels_kernel(LinkDev L) {
 // rounding (~1e-16 relative), not bit for bit.  Warp 0: loss, capacity, total
 // power; warp 1 + b: band b (bands beyond the warps loop).
 constexpr int kTotalsThreads = 256;
-constexpr int kMaxBands = 16;
 
 __device__ __forceinline__ double warp_sum_fixed(double v) {
 #pragma unroll
@@ -192,26 +177,6 @@ T* up(uwb_ctx* c, DBuf& b, const T* src, size_t n) {
 // Everything evaluate_link keeps resident between calls.
 }  // namespace uwb
 
-struct uwb_ctx::Prepared {
-  int n = 0;
-  int steps = 0;
-  int span_count = 1;
-  int include_raman = 1;
-  double rtol = 1e-9, atol = 1e-16, length = 0.0;
-  uwb_nli_cfg cfg{};
-  uwb::NliParams P{};
-  uwb::FinalizeParams F{};
-  uwb::OdeParams O{};
-  uwb::LinkDev L{};
-  int raman_n = 0;
-  double aeff_ref = 0.0;
-  const double* d_aeff = nullptr;
-  int* d_status = nullptr;
-  long long* d_rhs = nullptr;
-  double* d_psd = nullptr;  // the NLI/ODE/link read launch PSD from here
-  int grid_ctas = 0;
-  int launches = 0;
-};
 
 namespace uwb {
 
@@ -220,8 +185,6 @@ void release_link_state(uwb_ctx* c) {
   delete c->prep;
   c->prep = nullptr;
 }
-
-namespace {
 
 int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_cfg* lk,
             const uwb_nli_cfg* cfg) {
@@ -329,6 +292,10 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   P.counter = c->counter.get<unsigned int>(1);
   P.n_eval = c->n_eval.get<unsigned long long>(2);
   P.n_active = P.n_eval + 1;
+  P.probe_work = c->probe_work.get<unsigned long long>(std::max(np, 1));
+  c->last_n_probes = np;
+  c->last_probes_per_chan = cfg->simpson ? 3 : 1;
+  c->last_chan_probe0 = cp;
   FinalizeParams& F = pr->F;
   F.n_probes = np;
   F.probe_gamma = up(c, c->probe_gamma, gam.data(), gam.size());
@@ -396,7 +363,6 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   L.rho_end = d_rho_end;
   L.nf_db = d_nf;
   L.band = d_band2;
-  if (lk->n_bands > kMaxBands) return fail(UWB_CONFIG_ERROR, "uwb: at most 16 bands");
   L.n_bands = std::max(lk->n_bands, 0);
   L.span_count = fb->span_count;
   L.use_snr_trx = lk->use_snr_trx;
@@ -408,7 +374,8 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
   pr->grid_ctas = c->sm_count * per_sm;
   if (!P.log2rho || !P.zedge || !P.zstart || !P.zmid || !P.width || !P.wlast || !P.probe_nu ||
-      !P.probe_chan || !P.hl2 || !P.rowsum || !P.counter || !P.n_eval || !F.probe_gamma ||
+      !P.probe_chan || !P.hl2 || !P.rowsum || !P.counter || !P.n_eval || !P.probe_work ||
+      !F.probe_gamma ||
       !F.probe_g || !F.probe_quad || !F.chan_probe0 || !F.eta || !F.nli_psd || !F.nli_power ||
       !F.quad || !F.skipped || !L.out || !d_freq || !pr->d_psd || !d_guard || !d_alpha ||
       !pr->d_aeff || !d_nf || !d_mid)
@@ -422,7 +389,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
 // Noise stage of one evaluation on the prepared state (solve_link_noise,
 // link_optimizer.hpp:181-190): Raman ODE + NLI for the context's channels.
 // psd_dev = launch PSD (device) or null to keep the prepared one.
-int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_status = true) {
+int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_status) {
   uwb_ctx::Prepared* pr = c->prep;
   int launches = 0;
   if (psd_dev && psd_dev != pr->d_psd)
@@ -450,7 +417,7 @@ int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_sta
 }
 
 // Report stage (assemble_link_report, link_optimizer.hpp:194-237).
-int run_report(uwb_ctx* c, cudaStream_t st, const LinkDev* Lp = nullptr) {
+int run_report(uwb_ctx* c, cudaStream_t st, const LinkDev* Lp) {
   LinkDev L = Lp ? *Lp : c->prep->L;
   link_channels_kernel<<<(L.n + 127) / 128, 128, 0, st>>>(L);
   link_totals_kernel<<<1, kTotalsThreads, 0, st>>>(L);
@@ -461,7 +428,7 @@ int run_report(uwb_ctx* c, cudaStream_t st, const LinkDev* Lp = nullptr) {
   return UWB_OK;
 }
 
-int run_prepared(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_status = true) {
+int run_prepared(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_status) {
   int rc = run_noise(c, psd_dev, st, reset_status);
   if (rc) return rc;
   const int l = c->last_launches;
@@ -481,7 +448,6 @@ int check_status(uwb_ctx* c) {
   }
 }
 
-}  // namespace
 }  // namespace uwb
 
 using namespace uwb;
@@ -491,12 +457,14 @@ extern "C" {
 int uwb_evaluate_link_prepare(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
                               const uwb_link_cfg* link, const uwb_nli_cfg* cfg) {
   if (!c) return fail(UWB_CONFIG_ERROR, "null context");
+  if (c->multi()) return multi_prepare(c, grid, fibre, link, cfg, true);
   cudaSetDevice(c->device);
   return prepare(c, grid, fibre, link, cfg);
 }
 
 int uwb_evaluate_link_resident(uwb_ctx* c, const double* psd_dev, double* report_dev,
                                void* stream) {
+  if (c && c->multi()) return multi_resident(c, psd_dev, report_dev, stream);
   if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
   cudaSetDevice(c->device);
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
@@ -523,6 +491,7 @@ static int ensure_batch_state(uwb_ctx* c) {
 
 int uwb_evaluate_link_many(uwb_ctx* c, int n_eval, const double* psd_host, double* loss_host,
                            double* report_host) {
+  if (c && c->multi()) return multi_many(c, n_eval, psd_host, loss_host, report_host);
   if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
   if (n_eval < 0 || (n_eval > 0 && !psd_host)) return fail(UWB_CONFIG_ERROR, "bad batch");
   cudaSetDevice(c->device);
@@ -554,6 +523,7 @@ int uwb_evaluate_link_many(uwb_ctx* c, int n_eval, const double* psd_host, doubl
     const int per_sm = pr->grid_ctas / c->sm_count;
     const int grid = std::max(1, pr->grid_ctas - per_sm);
     NliParams Pb[2] = {pr->P, pr->P};
+    Pb[0].probe_work = Pb[1].probe_work = nullptr;  // two evaluations in flight
     FinalizeParams Fb[2] = {pr->F, pr->F};
     OdeParams Ob[2] = {pr->O, pr->O};
     LinkDev Lb[2] = {pr->L, pr->L};
@@ -612,6 +582,7 @@ int uwb_evaluate_link_many(uwb_ctx* c, int n_eval, const double* psd_host, doubl
 int uwb_evaluate_link(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
                       const uwb_link_cfg* link, const uwb_nli_cfg* cfg, uwb_link_report* out) {
   if (!c) return fail(UWB_CONFIG_ERROR, "null context");
+  if (c->multi()) return multi_evaluate_link(c, grid, fibre, link, cfg, out);
   cudaSetDevice(c->device);
   reset_xfer(c);
   int rc = prepare(c, grid, fibre, link, cfg);
@@ -659,6 +630,9 @@ int uwb_evaluate_link(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
 }
 
 int uwb_evaluate_link_resident_noise(uwb_ctx* c, const double* psd_dev, void* stream) {
+  if (c && c->multi())
+    return fail(UWB_CONFIG_ERROR, "the split noise/report stages belong to one device; a multi-GPU "
+                                  "context gathers eta itself (uwb_evaluate_link_resident)");
   if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
   cudaSetDevice(c->device);
   reset_xfer(c);
@@ -666,6 +640,9 @@ int uwb_evaluate_link_resident_noise(uwb_ctx* c, const double* psd_dev, void* st
 }
 
 int uwb_evaluate_link_resident_report(uwb_ctx* c, double* report_dev, void* stream) {
+  if (c && c->multi())
+    return fail(UWB_CONFIG_ERROR, "the split noise/report stages belong to one device; a multi-GPU "
+                                  "context gathers eta itself (uwb_evaluate_link_resident)");
   if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
   cudaSetDevice(c->device);
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
@@ -680,12 +657,16 @@ int uwb_evaluate_link_resident_report(uwb_ctx* c, double* report_dev, void* stre
 }
 
 int uwb_report_len(uwb_ctx* c, int* len) {
+  if (c && c->multi()) return uwb_report_len(c->subs[0], len);
   if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
   if (len) *len = 4 * c->prep->n + 3 + 2 * c->prep->L.n_bands;
   return UWB_OK;
 }
 
 int uwb_link_eta_buffer(uwb_ctx* c, double** eta_dev, int* n_ch) {
+  if (c && c->multi())
+    return fail(UWB_CONFIG_ERROR, "the split noise/report stages belong to one device; a multi-GPU "
+                                  "context gathers eta itself (uwb_evaluate_link_resident)");
   if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
   if (eta_dev) *eta_dev = c->prep->F.eta;
   if (n_ch) *n_ch = c->prep->n;
@@ -693,6 +674,7 @@ int uwb_link_eta_buffer(uwb_ctx* c, double** eta_dev, int* n_ch) {
 }
 
 int uwb_last_ode_stats(uwb_ctx* c, double* ode_ms, long long* rhs_evals) {
+  if (c && c->multi()) return uwb_last_ode_stats(c->subs[0], ode_ms, rhs_evals);
   if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
   uwb_ctx::Prepared* pr = c->prep;
   float ms = 0.f;
@@ -707,6 +689,7 @@ int uwb_last_ode_stats(uwb_ctx* c, double* ode_ms, long long* rhs_evals) {
 }
 
 int uwb_resident_status(uwb_ctx* c) {
+  if (c && c->multi()) return multi_status(c);
   if (!c || !c->prep) return fail(UWB_CONFIG_ERROR, "uwb_evaluate_link_prepare not called");
   return check_status(c);
 }
@@ -715,6 +698,7 @@ int uwb_power_evolution(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre
                         const uwb_link_cfg* link, int steps, const double* mid, double* log_rho,
                         double* rho_end) {
   if (!c) return fail(UWB_CONFIG_ERROR, "null context");
+  if (c->multi()) return uwb_power_evolution(c->subs[0], grid, fibre, link, steps, mid, log_rho, rho_end);
   cudaSetDevice(c->device);
   release_link_state(c);  // shares buffers with the prepared evaluation
   reset_xfer(c);

@@ -257,16 +257,31 @@ def gamma_at(fibre: FibreSpec, lambda_m) -> np.ndarray:
 
 # ----------------------------------------------------------------- engine
 class Engine:
-    """One CUDA context (device buffers resident in HBM across calls)."""
+    """One CUDA context (device buffers resident in HBM across calls).
 
-    def __init__(self, device: int | None = None):
+    ``devices=[d0, d1, ...]`` makes a multi-GPU context (uwb_ctx_create_multi):
+    the reference's worker pool (GnSolverConfig.workers) with GPUs as the
+    workers -- channels split over the devices for single evaluations,
+    whole evaluations dealt for batches, results bit-identical to one GPU.
+    """
+
+    def __init__(self, device: int | None = None, devices=None):
         self.lib = N.load()
-        if device is None:
-            device = int(os.environ.get("LOCAL_RANK", "0")) if "UWB_DEVICE" not in os.environ \
-                else int(os.environ["UWB_DEVICE"])
-        self.device = device
         h = N.C.c_void_p()
-        N.check(self.lib.uwb_ctx_create(int(device), N.C.byref(h)))
+        if devices is not None:
+            dv = np.ascontiguousarray(devices, dtype=np.int32)
+            if dv.size < 1:
+                raise ConfigError("need at least one device")
+            self.device = int(dv[0])
+            self.devices = [int(x) for x in dv]
+            N.check(self.lib.uwb_ctx_create_multi(N.iptr(dv), int(dv.size), N.C.byref(h)))
+        else:
+            if device is None:
+                device = int(os.environ.get("LOCAL_RANK", "0")) if "UWB_DEVICE" not in os.environ \
+                    else int(os.environ["UWB_DEVICE"])
+            self.device = device
+            self.devices = [int(device)]
+            N.check(self.lib.uwb_ctx_create(int(device), N.C.byref(h)))
         self.h = h
 
     def close(self):
@@ -283,6 +298,27 @@ class Engine:
     def set_channel_subset(self, channels):
         ch = np.ascontiguousarray(channels if channels is not None else [], dtype=np.int32)
         N.check(self.lib.uwb_set_channel_subset(self.h, len(ch), N.iptr(ch)))
+
+    def width(self):
+        """Devices behind this context."""
+        n = N.C.c_int()
+        N.check(self.lib.uwb_ctx_width(self.h, N.C.byref(n)))
+        return n.value
+
+    def last_channel_work(self, n_ch):
+        """|K|^2 evaluations per channel of the last NLI (the split's cost model)."""
+        w = np.zeros(n_ch)
+        N.check(self.lib.uwb_last_channel_work(self.h, int(n_ch), N.dptr(w)))
+        return w
+
+    def last_partition_stats(self):
+        """Per device of the last split evaluation: integrand / ODE ms and the
+        first channel of its range."""
+        n = self.width()
+        a, b = np.zeros(n), np.zeros(n)
+        f = np.zeros(n, np.int32)
+        N.check(self.lib.uwb_last_partition_stats(self.h, n, N.dptr(a), N.dptr(b), N.iptr(f)))
+        return dict(nli_ms=a.tolist(), ode_ms=b.tolist(), first_channel=f.tolist())
 
     def device_info(self):
         a, b, c = N.C.c_int(), N.C.c_int(), N.C.c_int()

@@ -32,6 +32,22 @@ def test_cxx_shim_parity():
     assert "0 failure(s)" in r.stdout
 
 
+@pytest.mark.gpu
+def test_cxx_shim_parity_multi_gpu_workers():
+    """The same restated reference assertions with the drop-in's worker pool
+    mapped to GPUs: UWB_DEVICES=0,0,0 gives three contexts on the one test
+    GPU, so every all_channels_nli / evaluate_link with workers = 0 (all) or
+    4 runs the multi-GPU split (uwb_ctx_create_multi) -- the reference's
+    bit-identity across worker counts (test_gn_integral.cpp:291-300) must hold."""
+    if not os.path.exists(BIN):
+        pytest.skip("oracle/_ref/shim_parity not built (needs /root/reference at build time)")
+    env = dict(os.environ, UWB_DEVICES="0,0,0")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=900, env=env)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failure(s)" in r.stdout
+
+
 OPT = os.path.join(ROOT, "oracle", "_ref", "optimise_b200")
 
 
