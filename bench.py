@@ -226,6 +226,9 @@ def run_engine(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
+        # NCCL's INIT lines let the driver count the ranks of the communicator
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     eng = uwb.Engine(local)
@@ -259,6 +262,16 @@ def run_engine(args):
         step()
     torch.cuda.synchronize(dev)
     res.check_status()
+    if world > 1:
+        # re-deal the channels by LPT on the per-channel work every rank
+        # measured in the warm-up (one all-reduce), then warm the new split
+        sh.rebalance()
+        res = sh.res
+        report = torch.zeros(sh.report_len, dtype=torch.float64, device=dev)
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize(dev)
+        res.check_status()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -283,6 +296,7 @@ def run_engine(args):
     t = torch.tensor([total_ms, float(np.mean(kern_ms)), float(np.mean(ode_ms)), stats["inner_steps"],
                       stats["active_points"] * stats["inner_steps"] / max(stats["evaluated_points"], 1.0)],
                      dtype=torch.float64, device=dev)
+    per_rank = None
     if world > 1:
         tmax = t.clone()
         dist.all_reduce(tmax[:3], op=dist.ReduceOp.MAX)
@@ -290,6 +304,18 @@ def run_engine(args):
         dist.all_reduce(tsum[3:], op=dist.ReduceOp.SUM)
         total_ms, kmax, omax = float(tmax[0]), float(tmax[1]), float(tmax[2])
         inner, inner_ref = float(tsum[3]), float(tsum[4])
+        # per-rank integrand / ODE device time and channel count
+        mine = torch.tensor([float(np.mean(kern_ms)), float(np.mean(ode_ms)), float(len(sh.mine))],
+                            dtype=torch.float64, device=dev)
+        allr = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        allr = [a.cpu().numpy() for a in allr]
+        nli_r = [float(a[0]) for a in allr]
+        per_rank = {"nli_ms": nli_r, "ode_ms": [float(a[1]) for a in allr],
+                    "channels": [int(a[2]) for a in allr],
+                    "nli_max_over_min": max(nli_r) / min(nli_r) if min(nli_r) > 0 else None,
+                    "partition": "LPT on per-channel work measured in the warm-up "
+                                 "(uwb_last_channel_work, all-reduced)"}
     else:
         kmax, omax, inner, inner_ref = float(t[1]), float(t[2]), float(t[3]), float(t[4])
     ms_per = total_ms / args.steps
@@ -474,6 +500,7 @@ def run_engine(args):
             "variants": variants,
             "result_check": {"loss": float(rep[4 * n]), "total_capacity_tbps": float(rep[4 * n + 1]) / 1e12},
             "parity": headline_parity(rep, n, args),
+            "per_rank": per_rank,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

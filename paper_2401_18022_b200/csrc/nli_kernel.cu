@@ -626,7 +626,10 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
     // prepared path: the probe's channel is dark in this evaluation -> the
     // reference skips it (gn_integral.hpp:349-352); its rows add nothing
     if (P.probe_chan && !(__ldg(P.psd + __ldg(P.probe_chan + probe)) > 0.0)) {
-      if (lane == 0) P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
+      if (lane == 0) {
+        P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
+        P.rowcnt[row] = make_uint2(0u, 0u);
+      }
       continue;
     }
     if (HOIST && probe != cur_probe) {
@@ -653,7 +656,10 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
       }
       const double u1_max = b1 * b2;
       if (!(u1_max > 0.0)) {
-        if (lane == 0) P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
+        if (lane == 0) {
+          P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
+          P.rowcnt[row] = make_uint2(0u, 0u);
+        }
         continue;
       }
       // u1 bin (gn_integral.hpp:262-286)
@@ -671,7 +677,10 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
       const double hi = log(b1 / su);
       const double lo = -log(b2 / su);
       if (!(hi > lo)) {
-        if (lane == 0) P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
+        if (lane == 0) {
+          P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
+          P.rowcnt[row] = make_uint2(0u, 0u);
+        }
         continue;
       }
       __syncwarp();
@@ -780,9 +789,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
       double acc = 0.0;
       for (int t = 0; t < n_r; ++t) acc += val_row[t];  // ascending j (gn_integral.hpp:288-305)
       P.rowsum[row] = acc * du1 * S.du2;
-      atomicAdd(P.n_eval, static_cast<unsigned long long>(n_eval));
-      atomicAdd(P.n_active, static_cast<unsigned long long>(n_act_row));
-      if (P.probe_work) atomicAdd(P.probe_work + probe, static_cast<unsigned long long>(n_eval));
+      P.rowcnt[row] = make_uint2(n_eval, n_act_row);  // summed per probe by the finalize
     }
     __syncwarp();
 
@@ -818,10 +825,27 @@ __global__ void finalize_probes_kernel(const NliParams P, const FinalizeParams F
   const int probe = blockIdx.x;
   const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ double quad[4];
+  __shared__ unsigned long long cnt[4][2];
   if (q < P.n_q) {
     double* rs_s = fin_smem + q * P.n_r;
     const double* rs = P.rowsum + (static_cast<size_t>(probe) * P.n_q + q) * P.n_r;
-    for (int i = lane; i < P.n_r; i += 32) rs_s[i] = rs[i];
+    const uint2* rc = P.rowcnt + (static_cast<size_t>(probe) * P.n_q + q) * P.n_r;
+    unsigned long long ce = 0, ca = 0;
+    for (int i = lane; i < P.n_r; i += 32) {
+      rs_s[i] = rs[i];
+      const uint2 c2 = rc[i];
+      ce += c2.x;
+      ca += c2.y;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      ce += __shfl_xor_sync(0xffffffffu, ce, o);
+      ca += __shfl_xor_sync(0xffffffffu, ca, o);
+    }
+    if (lane == 0) {
+      cnt[q][0] = ce;
+      cnt[q][1] = ca;
+    }
     __syncwarp();
     if (lane == 0) {
       double sum = 0.0, comp = 0.0;
@@ -837,9 +861,16 @@ __global__ void finalize_probes_kernel(const NliParams P, const FinalizeParams F
     }
   } else if (lane == 0 && q < 4) {
     quad[q] = 0.0;
+    cnt[q][0] = cnt[q][1] = 0;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    // work counters: one atomic per probe (not per row)
+    const unsigned long long ce = cnt[0][0] + cnt[1][0] + cnt[2][0] + cnt[3][0];
+    const unsigned long long ca = cnt[0][1] + cnt[1][1] + cnt[2][1] + cnt[3][1];
+    atomicAdd(P.n_eval, ce);
+    atomicAdd(P.n_active, ca);
+    if (P.probe_work) P.probe_work[probe] = ce;
     double qd[4] = {quad[0], quad[1], quad[2], P.n_q > 3 ? quad[3] : 0.0};
     if (F.mirror_q4) qd[3] = qd[1];
     const double g = F.probe_gamma[probe];
@@ -1041,7 +1072,6 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
   int launches = 0;
   cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), stream);
   cudaMemsetAsync(p.n_eval, 0, 2 * sizeof(unsigned long long), stream);  // n_eval, n_active
-  if (p.probe_work) cudaMemsetAsync(p.probe_work, 0, p.n_probes * sizeof(unsigned long long), stream);
   probe_halflog_kernel<<<p.n_probes, 128, 0, stream>>>(p);
   ++launches;
   if (ev_k0) cudaEventRecord(ev_k0, stream);

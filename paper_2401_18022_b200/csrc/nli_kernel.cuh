@@ -60,6 +60,7 @@ struct NliParams {
   unsigned int* counter;        // row queue head (zeroed before launch)
   unsigned long long* n_eval;   // [2]: |K|^2 evaluations, active points (stats)
   unsigned long long* n_active; // = n_eval + 1
+  uint2* rowcnt;                // [total_rows] (|K|^2 evaluations, active points) per row
   unsigned long long* probe_work;  // [n_probes] |K|^2 evaluations per probe (null: off);
                                   // the multi-GPU partition's cost model
   int mirror_u2;                // share |K|^2 across u2 -> -u2 in symmetric rows

@@ -60,6 +60,7 @@ struct uwb_ctx {
   uwb::DBuf log2rho, zedge, zstart, zmid, width, wlast;
   // probes + work
   uwb::DBuf probe_work;  // per-probe |K|^2 evaluations of the last NLI
+  uwb::DBuf rowcnt;      // per-row work counts (summed per probe by the finalize)
   uwb::DBuf probe_nu, probe_chan, probe_gamma, hl2, rowsum, counter, n_eval, probe_g, probe_quad, chan_probe0;
   // per-channel results
   uwb::DBuf eta, nli_psd, nli_power, quad, skipped;

@@ -293,6 +293,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   P.n_eval = c->n_eval.get<unsigned long long>(2);
   P.n_active = P.n_eval + 1;
   P.probe_work = c->probe_work.get<unsigned long long>(std::max(np, 1));
+  P.rowcnt = c->rowcnt.get<uint2>(std::max(P.total_rows, 1));
   c->last_n_probes = np;
   c->last_probes_per_chan = cfg->simpson ? 3 : 1;
   c->last_chan_probe0 = cp;
@@ -374,7 +375,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
   pr->grid_ctas = c->sm_count * per_sm;
   if (!P.log2rho || !P.zedge || !P.zstart || !P.zmid || !P.width || !P.wlast || !P.probe_nu ||
-      !P.probe_chan || !P.hl2 || !P.rowsum || !P.counter || !P.n_eval || !P.probe_work ||
+      !P.probe_chan || !P.hl2 || !P.rowsum || !P.counter || !P.n_eval || !P.probe_work || !P.rowcnt ||
       !F.probe_gamma ||
       !F.probe_g || !F.probe_quad || !F.chan_probe0 || !F.eta || !F.nli_psd || !F.nli_power ||
       !F.quad || !F.skipped || !L.out || !d_freq || !pr->d_psd || !d_guard || !d_alpha ||

@@ -14,8 +14,13 @@ GPUs:
 * the SNR report is then assembled on every rank from the full vector.
 
 Partitioning: channels are dealt by longest-processing-time (LPT) on a cost
-model (default: uniform -- adjacent channels have near-equal cost, so a
-round-robin deal balances to ~1 %).
+model.  The first evaluation deals round-robin; ShardedLink.rebalance() then
+takes the per-channel work every rank measured on its device (|K|^2
+evaluations per channel, uwb_last_channel_work: the active points and the
+heavier MCI-region channels near lambda_0), sums it over the
+ranks with one all-reduce, and re-deals by LPT.  The C-ABI's own multi-GPU
+context (uwb_ctx_create_multi, one process driving several GPUs) uses the same
+measured cost with contiguous ranges.
 """
 from __future__ import annotations
 
@@ -71,16 +76,24 @@ class ShardedLink:
     """
 
     def __init__(self, fibre, grid, cfg, rank: int, world: int, engine=None, cost=None):
+        self.rank, self.world = rank, world
+        self.fibre, self.grid, self.cfg = fibre, grid, cfg
+        from .gn_integral import get_engine
+
+        self.eng = engine or get_engine()
+        self._setup(cost)
+
+    def _setup(self, cost):
         import torch
 
-        from .gn_integral import ResidentLink, get_engine
+        from .gn_integral import ResidentLink
 
-        self.rank, self.world = rank, world
-        self.eng = engine or get_engine()
-        self.parts = partition_channels(active_channels(grid), world, cost)
+        grid, world, rank = self.grid, self.world, self.rank
+        act = active_channels(grid)
+        self.parts = partition_channels(act, world, None if cost is None else np.asarray(cost)[act])
         self.mine = self.parts[rank]
         self.eng.set_channel_subset(self.mine if world > 1 else None)
-        self.res = ResidentLink(fibre, grid, cfg, engine=self.eng)
+        self.res = ResidentLink(self.fibre, grid, self.cfg, engine=self.eng)
         ptr, n = self.res.eta_buffer()
         dev = torch.device("cuda", torch.cuda.current_device())
 
@@ -90,6 +103,30 @@ class ShardedLink:
 
         self.eta = torch.as_tensor(_Cai(), device=dev)
         self.report_len = self.res.report_len
+
+    def rebalance(self):
+        """Re-deal the channels by LPT on the per-channel work the last
+        evaluation measured on every rank (one all-reduce of the cost
+        vector).  Results do not change -- only the balance."""
+        import torch
+        import torch.distributed as dist
+
+        n = self.grid.size()
+        w = torch.tensor(self.eng.last_channel_work(n), dtype=torch.float64,
+                         device=self.eta.device)
+        if self.world > 1 and dist.is_available() and dist.is_initialized():
+            dist.all_reduce(w, op=dist.ReduceOp.SUM)
+        self.cost = w.cpu().numpy()
+        self._setup(self.cost)
+        return self.cost
+
+    def balance(self):
+        """max / mean of the measured cost over the ranks' shares (1.0 = even)."""
+        c = getattr(self, "cost", None)
+        if c is None:
+            return None
+        loads = [float(np.sum(c[p])) for p in self.parts]
+        return max(loads) / (sum(loads) / len(loads)) if sum(loads) > 0 else None
 
     def run(self, psd_ptr: int, report_ptr: int, stream_ptr: int) -> int:
         """One evaluation; returns the number of engine kernel launches."""

@@ -108,8 +108,15 @@ def _gpu_worker(rank, world, port, q):
         sh.run(psd.data_ptr(), rep.data_ptr(), st.cuda_stream)
     torch.cuda.synchronize()
     sh.check_status()
+    first = rep.cpu().numpy().copy()
+    # re-deal by LPT on the per-channel work both ranks measured, run again
+    cost = sh.rebalance()
+    with torch.cuda.stream(st):
+        sh.run(psd.data_ptr(), rep.data_ptr(), st.cuda_stream)
+    torch.cuda.synchronize()
+    sh.check_status()
     if rank == 0:
-        q.put(rep.cpu().numpy().copy())
+        q.put((first, rep.cpu().numpy().copy(), float(np.sum(cost)), sh.balance()))
     dist.barrier()
     dist.destroy_process_group()
     eng.close()
@@ -125,7 +132,7 @@ def test_two_rank_sharded_link_matches_single_gpu():
     procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    got = q.get(timeout=300)
+    got, again, total_work, balance = q.get(timeout=300)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
@@ -139,3 +146,7 @@ def test_two_rank_sharded_link_matches_single_gpu():
     assert np.array_equal(got[:n], one.eta)          # bit-identical eta
     assert np.array_equal(got[2 * n:3 * n], one.snr_db)
     assert got[4 * n] == one.loss_value
+    # the cost-balanced (LPT on measured per-channel work) re-deal changes
+    # nothing but the balance
+    assert np.array_equal(again, got)
+    assert total_work > 0 and balance is not None and balance < 1.01
