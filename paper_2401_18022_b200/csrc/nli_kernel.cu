@@ -326,12 +326,15 @@ __device__ __forceinline__ void mixed_sincos(double x, float* c_out, float* s_ou
 // m >= N (only when N < 16 K) mask p to 0 and feed sincos a 0 angle.
 // HOIST: the lane's K end-edge positions Zr and probe half-logs Hr live in
 // registers for the whole row (single span, K <= 8).
+// K = 0: steps per lane known only at run time (spans longer than 512
+// steps): the same code with rolled step loops.
 template <int K, bool FULL, bool HOIST, bool TINY>
 __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSmem& S, int idx,
                                                int probe, int sl, unsigned segmask,
-                                               const double (&Zr)[K], const double (&Hr)[K]) {
-  constexpr int NS = 16 * K;
-  const int N = P.steps;
+                                               const double (&Zr)[K > 0 ? K : 1],
+                                               const double (&Hr)[K > 0 ? K : 1]) {
+  const int Kr = K > 0 ? K : P.col_stride / 16;
+  const int NS = 16 * Kr;
   const PointRec& R = S.pt[idx];
   const double2 wa = *reinterpret_cast<const double2*>(&R.w[0]);
   const double2 wb = *reinterpret_cast<const double2*>(&R.w[2]);
@@ -344,6 +347,8 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
   double fre = 0.0, fim = 0.0, sre = 0.0, sim = 0.0;
   const int n_spans = HOIST ? 1 : P.n_spans;
   for (int k = 0; k < n_spans; ++k) {
+    // this span's own step count (spans may differ, gn_integral.hpp:231-251)
+    const int N = (HOIST || !P.span_steps) ? P.steps : __ldg(P.span_steps + k);
     const double* T = P.log2rho + k * P.span_stride;
     const double* ca = T + oa;
     const double* cb = T + ob;
@@ -353,8 +358,8 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
     if (fast) {
       const double* ze = P.zedge + static_cast<size_t>(k) * NS + sl;
       double p0 = 0.0, pp = 0.0, pc = 0.0, ps = 0.0;
-#pragma unroll
-      for (int b = 0; b < K; ++b) {
+#pragma unroll(K > 0 ? K : 4)
+      for (int b = 0; b < Kr; ++b) {
         const int o = 16 * b;
         const double H = HOIST ? Hr[b] : __ldg(hl + o);
         const double Z = HOIST ? Zr[b] : __ldg(ze + o);
@@ -367,7 +372,7 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
         double p = step_exp2_16(lg);
         double ang = phi * Z;
         if (!FULL) {
-          const bool ok = sl * K + b < N;
+          const bool ok = sl * Kr + b < N;
           p = ok ? p : 0.0;
           ang = ok ? ang : 0.0;
         }
@@ -413,8 +418,8 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
       // Taylor kernels to x^6 / x^7 are exact to < 1e-19 and replace the
       // reduction + table sincos (8 FP64 instructions instead of 19).  Each
       // kernel holds one of the two loops (both in one kernel cost 4 %).
-#pragma unroll
-      for (int b = 0; b < K; ++b) {
+#pragma unroll(K > 0 ? K : 4)
+      for (int b = 0; b < Kr; ++b) {
         const int o = 16 * b;
         const double H = HOIST ? Hr[b] : __ldg(hl + o);
         double lg = fma(w0, __ldg(ca + o), -H);
@@ -430,7 +435,7 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
         const double x2 = x * x;
         const double sinc = fma(x2, fma(x2, 1.0 / 120.0, -1.0 / 6.0), 1.0);
         double w = p * wm * sinc;
-        if (!FULL) w = (sl * K + b < N) ? w : 0.0;
+        if (!FULL) w = (sl * Kr + b < N) ? w : 0.0;
         const double a = phi * __ldg(zm + o);
         double cs, sn;
         if constexpr (TINY) {
@@ -465,7 +470,6 @@ __device__ __forceinline__ double point_kernel_mixed(const NliParams& P, const W
                                                      int probe, int sl, unsigned segmask,
                                                      const double (&Zr)[K], const double (&Hr)[K]) {
   constexpr int NS = 16 * K;
-  const int N = P.steps;
   const PointRec& R = S.pt[idx];
   const double2 wa = *reinterpret_cast<const double2*>(&R.w[0]);
   const double2 wb = *reinterpret_cast<const double2*>(&R.w[2]);
@@ -478,6 +482,7 @@ __device__ __forceinline__ double point_kernel_mixed(const NliParams& P, const W
   double fre = 0.0, fim = 0.0, sre = 0.0, sim = 0.0;
   const int n_spans = HOIST ? 1 : P.n_spans;
   for (int k = 0; k < n_spans; ++k) {
+    const int N = (HOIST || !P.span_steps) ? P.steps : __ldg(P.span_steps + k);
     const double* T = P.log2rho + k * P.span_stride;
     const double* ca = T + oa;
     const double* cb = T + ob;
@@ -602,7 +607,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
   }
   __syncthreads();
 
-  constexpr int NS = 16 * K;
+  const int NS = 16 * (K > 0 ? K : P.col_stride / 16);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int sl = lane & 15;
@@ -610,7 +615,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
   const unsigned segmask = 0xffffu << (16 * seg);
   WarpSmem& S = s_w[warp];
   const int per_probe = P.n_q * P.n_r;
-  double Zr[K], Hr[K];
+  double Zr[K > 0 ? K : 1], Hr[K > 0 ? K : 1];
   int cur_probe = -1;
   if (HOIST) {
 #pragma unroll
@@ -776,9 +781,11 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
       for (int base = 0; base < n_need; base += 2) {
         const bool ok = base + seg < n_need;
         const int idx = ok ? base + seg : base;
-        const double kv =
-            MIXED ? point_kernel_mixed<K, FULL, HOIST>(P, S, idx, probe, sl, segmask, Zr, Hr)
-                  : point_kernel<K, FULL, HOIST, TINY>(P, S, idx, probe, sl, segmask, Zr, Hr);
+        double kv;
+        if constexpr (MIXED)
+          kv = point_kernel_mixed<K, FULL, HOIST>(P, S, idx, probe, sl, segmask, Zr, Hr);
+        else
+          kv = point_kernel<K, FULL, HOIST, TINY>(P, S, idx, probe, sl, segmask, Zr, Hr);
         if (ok && sl == 0) S.kv[S.pt[idx].src] = kv;
       }
       __syncwarp();
@@ -904,69 +911,74 @@ __global__ void finalize_channels_kernel(const FinalizeParams F) {
 
 using RowKernel = void (*)(const NliParams);
 
+// full: every span has exactly 16 K steps (no masked lanes).
 template <int K, bool MIXED>
-RowKernel pick2(int steps, bool one_span, bool tiny) {
+RowKernel pick2(bool full, bool one_span, bool tiny) {
   constexpr bool kHoist = K <= 8;
   if (one_span && kHoist) {
     if (!MIXED && tiny)
-      return steps == 16 * K ? nli_rows_kernel<K, true, kHoist, MIXED, !MIXED>
-                             : nli_rows_kernel<K, false, kHoist, MIXED, !MIXED>;
-    return steps == 16 * K ? nli_rows_kernel<K, true, kHoist, MIXED, false>
-                           : nli_rows_kernel<K, false, kHoist, MIXED, false>;
+      return full ? nli_rows_kernel<K, true, kHoist, MIXED, !MIXED>
+                  : nli_rows_kernel<K, false, kHoist, MIXED, !MIXED>;
+    return full ? nli_rows_kernel<K, true, kHoist, MIXED, false>
+                : nli_rows_kernel<K, false, kHoist, MIXED, false>;
   }
-  return steps == 16 * K ? nli_rows_kernel<K, true, false, MIXED, false>
-                         : nli_rows_kernel<K, false, false, MIXED, false>;
+  return full ? nli_rows_kernel<K, true, false, MIXED, false>
+              : nli_rows_kernel<K, false, false, MIXED, false>;
 }
 
 template <int K>
-RowKernel pick(int steps, bool one_span, bool mixed, bool tiny) {
-  return mixed ? pick2<K, true>(steps, one_span, tiny) : pick2<K, false>(steps, one_span, tiny);
+RowKernel pick(bool full, bool one_span, bool mixed, bool tiny) {
+  return mixed ? pick2<K, true>(full, one_span, tiny) : pick2<K, false>(full, one_span, tiny);
 }
 
 // Long spans (257..512 steps, e.g. 80 km at > 3.2 steps/km): FP64, per-step
 // z / half-log loads (no hoisting at this K); the compensated-FP32 mode stops
 // at 256 steps.
 template <int K>
-RowKernel pick_long(int steps, bool mixed) {
+RowKernel pick_long(bool full, bool mixed) {
   if (mixed) return nullptr;
-  return steps == 16 * K ? nli_rows_kernel<K, true, false, false, false>
-                         : nli_rows_kernel<K, false, false, false, false>;
+  return full ? nli_rows_kernel<K, true, false, false, false>
+              : nli_rows_kernel<K, false, false, false, false>;
 }
 
-RowKernel row_kernel_for(int steps, bool one_span, bool mixed, bool tiny) {
-  switch ((steps + 15) / 16) {
-    case 1: return pick<1>(steps, one_span, mixed, tiny);
-    case 2: return pick<2>(steps, one_span, mixed, tiny);
-    case 3: return pick<3>(steps, one_span, mixed, tiny);
-    case 4: return pick<4>(steps, one_span, mixed, tiny);
-    case 5: return pick<5>(steps, one_span, mixed, tiny);
-    case 6: return pick<6>(steps, one_span, mixed, tiny);
-    case 7: return pick<7>(steps, one_span, mixed, tiny);
-    case 8: return pick<8>(steps, one_span, mixed, tiny);
-    case 9: return pick<9>(steps, one_span, mixed, tiny);
-    case 10: return pick<10>(steps, one_span, mixed, tiny);
-    case 11: return pick<11>(steps, one_span, mixed, tiny);
-    case 12: return pick<12>(steps, one_span, mixed, tiny);
-    case 13: return pick<13>(steps, one_span, mixed, tiny);
-    case 14: return pick<14>(steps, one_span, mixed, tiny);
-    case 15: return pick<15>(steps, one_span, mixed, tiny);
-    case 16: return pick<16>(steps, one_span, mixed, tiny);
-    case 17: return pick_long<17>(steps, mixed);
-    case 18: return pick_long<18>(steps, mixed);
-    case 19: return pick_long<19>(steps, mixed);
-    case 20: return pick_long<20>(steps, mixed);
-    case 21: return pick_long<21>(steps, mixed);
-    case 22: return pick_long<22>(steps, mixed);
-    case 23: return pick_long<23>(steps, mixed);
-    case 24: return pick_long<24>(steps, mixed);
-    case 25: return pick_long<25>(steps, mixed);
-    case 26: return pick_long<26>(steps, mixed);
-    case 27: return pick_long<27>(steps, mixed);
-    case 28: return pick_long<28>(steps, mixed);
-    case 29: return pick_long<29>(steps, mixed);
-    case 30: return pick_long<30>(steps, mixed);
-    case 31: return pick_long<31>(steps, mixed);
-    case 32: return pick_long<32>(steps, mixed);
+// steps: the longest span's step count; ragged: spans differ in step count.
+RowKernel row_kernel_for(int steps, bool one_span, bool mixed, bool tiny, bool ragged = false) {
+  const int K = (steps + 15) / 16;
+  const bool full = steps == 16 * K && !ragged;
+  if (K > 32) return mixed ? nullptr : nli_rows_kernel<0, false, false, false, false>;
+  switch (K) {
+    case 1: return pick<1>(full, one_span, mixed, tiny);
+    case 2: return pick<2>(full, one_span, mixed, tiny);
+    case 3: return pick<3>(full, one_span, mixed, tiny);
+    case 4: return pick<4>(full, one_span, mixed, tiny);
+    case 5: return pick<5>(full, one_span, mixed, tiny);
+    case 6: return pick<6>(full, one_span, mixed, tiny);
+    case 7: return pick<7>(full, one_span, mixed, tiny);
+    case 8: return pick<8>(full, one_span, mixed, tiny);
+    case 9: return pick<9>(full, one_span, mixed, tiny);
+    case 10: return pick<10>(full, one_span, mixed, tiny);
+    case 11: return pick<11>(full, one_span, mixed, tiny);
+    case 12: return pick<12>(full, one_span, mixed, tiny);
+    case 13: return pick<13>(full, one_span, mixed, tiny);
+    case 14: return pick<14>(full, one_span, mixed, tiny);
+    case 15: return pick<15>(full, one_span, mixed, tiny);
+    case 16: return pick<16>(full, one_span, mixed, tiny);
+    case 17: return pick_long<17>(full, mixed);
+    case 18: return pick_long<18>(full, mixed);
+    case 19: return pick_long<19>(full, mixed);
+    case 20: return pick_long<20>(full, mixed);
+    case 21: return pick_long<21>(full, mixed);
+    case 22: return pick_long<22>(full, mixed);
+    case 23: return pick_long<23>(full, mixed);
+    case 24: return pick_long<24>(full, mixed);
+    case 25: return pick_long<25>(full, mixed);
+    case 26: return pick_long<26>(full, mixed);
+    case 27: return pick_long<27>(full, mixed);
+    case 28: return pick_long<28>(full, mixed);
+    case 29: return pick_long<29>(full, mixed);
+    case 30: return pick_long<30>(full, mixed);
+    case 31: return pick_long<31>(full, mixed);
+    case 32: return pick_long<32>(full, mixed);
     default: return nullptr;
   }
 }
@@ -1050,8 +1062,8 @@ void allow_row_smem(RowKernel k, int n_r) {
 }
 }  // namespace
 
-int nli_ctas_per_sm(int steps, bool one_span, int n_r, bool mixed, bool tiny) {
-  RowKernel k = row_kernel_for(steps, one_span, mixed, tiny);
+int nli_ctas_per_sm(int steps, bool one_span, int n_r, bool mixed, bool tiny, bool ragged) {
+  RowKernel k = row_kernel_for(steps, one_span, mixed, tiny, ragged);
   if (!k) return 0;
   allow_row_smem(k, n_r);
   int n = 0;
@@ -1067,7 +1079,8 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
     const char* e = std::getenv("UWB_NLI_NO_HOIST");
     return e && e[0] == '1';
   }();
-  RowKernel k = row_kernel_for(p.steps, p.n_spans == 1 && !no_hoist, p.mixed != 0, p.slow_tiny != 0);
+  RowKernel k = row_kernel_for(p.steps, p.n_spans == 1 && !no_hoist, p.mixed != 0, p.slow_tiny != 0,
+                               p.span_steps != nullptr);
   if (!k || p.n_probes <= 0 || p.col_stride != 16 * ((p.steps + 15) / 16)) return -1;
   int launches = 0;
   cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), stream);

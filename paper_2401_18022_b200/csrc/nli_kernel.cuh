@@ -29,7 +29,8 @@ struct NliParams {
   // ch*steps+m scaled by log2 e so the integrand can use exp2), span-absolute
   // step geometry, all in lane order.
   int n_spans;
-  int steps;
+  int steps;              // steps of the longest span (every span's when span_steps is null)
+  const int* span_steps;  // [n_spans] each span's own step count, or null (all equal)
   int col_stride;         // NS = 16 * ceil(steps / 16): padded column length (doubles)
   const double* log2rho;  // [n_spans][n_ch + 1][NS]: log2 rho, zero pad column n and pad steps
   size_t span_stride;     // (n_ch + 1) * NS, or 0 when every span shares one table
@@ -95,8 +96,9 @@ struct SpanTables {
   double zmid_max = 0.0;  // largest |z| of a step midpoint over all spans
 };
 inline void append_span_tables(const double* edge, const double* mid, const double* width,
-                               int steps, double z_base, SpanTables* t) {
-  const int K = (steps + 15) / 16, NS = 16 * K;
+                               int steps, double z_base, SpanTables* t, int NS = 0) {
+  if (NS <= 0) NS = 16 * ((steps + 15) / 16);  // else the longest span's padded length
+  const int K = NS / 16;
   const size_t o = t->zend.size();
   t->zend.resize(o + NS);
   t->zmid.resize(o + NS);
@@ -121,7 +123,8 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
                cudaEvent_t ev_k0, cudaEvent_t ev_k1);
 
 // CTAs per SM the integrand kernel reaches for a given step count.
-int nli_ctas_per_sm(int steps, bool one_span, int n_r, bool mixed = false, bool tiny = false);
+int nli_ctas_per_sm(int steps, bool one_span, int n_r, bool mixed = false, bool tiny = false,
+                    bool ragged = false);
 
 // Sinc-branch points have |phi| w_last <= 1e-4 (gn_integral.hpp:156), so their
 // phases satisfy |phi z| <= 1e-4 z_max / w_last; the Taylor sincos of the TINY
@@ -132,7 +135,9 @@ inline bool slow_tiny_ok(const SpanTables& t) {
     wmin = k == 0 ? t.wlast[k] : std::min(wmin, t.wlast[k]);
   return wmin > 0.0 && 1e-4 * t.zmid_max <= 0.015625 * wmin;
 }
-constexpr int kMaxSteps = 512;  // 16 lanes x 32 steps per lane
+// Steps per span: up to 512 (16 lanes x 32 unrolled steps per lane) take the
+// specialised kernels, longer spans the rolled K = 0 kernel.
+constexpr int kMaxSteps = 16 * 4096;
 // Elements allocated past the end of log2rho / zedge / hl2: the integrand's
 // lanes with m >= N load them and mask the result (branch-free tail).
 constexpr int kTablePad = 32;

@@ -90,15 +90,19 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   // nli_psd_at's checks, in the reference's order (gn_integral.hpp:223-240)
   if (n_spans <= 0 || !spans) return fail(UWB_CONFIG_ERROR, "nli_psd_at: need at least one span");
   const int n = g->n_ch;
-  const int steps = spans[0].steps;
+  // Each span keeps its own step count (the reference walks every span's own
+  // distance grid, gn_integral.hpp:231-251): the columns are padded to the
+  // longest span, and a span's lanes past its own count are masked.
+  int steps = 0;
+  bool ragged = false;
   for (int k = 0; k < n_spans; ++k) {
-    if (spans[k].steps != steps)
-      return fail(UWB_CONFIG_ERROR, "uwb: all spans must share one distance-step count");
     if (!spans[k].log_rho || !spans[k].edge || !spans[k].mid || !spans[k].width)
       return fail(UWB_CONFIG_ERROR, "nli_psd_at: span evolution does not match the channel grid");
+    if (spans[k].steps < 1 || spans[k].steps > kMaxSteps)
+      return fail(UWB_CONFIG_ERROR, "uwb: distance steps per span must be in [1, 65536]");
+    if (k > 0 && spans[k].steps != spans[0].steps) ragged = true;
+    steps = std::max(steps, spans[k].steps);
   }
-  if (steps < 1 || steps > kMaxSteps)
-    return fail(UWB_CONFIG_ERROR, "uwb: distance steps per span must be in [1, 512]");
 
   // Padded device layout (nli_kernel.cuh): columns NS = 16 ceil(N/16) long,
   // one zero pad column n per span, edges past N repeat the span end.
@@ -108,15 +112,26 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   SpanTables stb;
   const int K = NS / 16;
   double z_base = 0.0;
+  std::vector<int> span_steps(n_spans);
+  long long total_steps = 0;
   for (int k = 0; k < n_spans; ++k) {
     const uwb_span& s = spans[k];
+    const int sk = s.steps;
+    span_steps[k] = sk;
+    total_steps += sk;
     double* t = tab.data() + static_cast<size_t>(k) * cols;
     for (int ch = 0; ch < n; ++ch)
-      for (int m = 0; m < steps; ++m)
+      for (int m = 0; m < sk; ++m)
         t[static_cast<size_t>(ch) * NS + lane_pos(m, K)] =
-            s.log_rho[static_cast<size_t>(ch) * steps + m] * kLog2e;
-    append_span_tables(s.edge, s.mid, s.width, steps, z_base, &stb);
+            s.log_rho[static_cast<size_t>(ch) * sk + m] * kLog2e;
+    append_span_tables(s.edge, s.mid, s.width, sk, z_base, &stb, NS);
     z_base += s.length;
+  }
+  int* d_ss = nullptr;
+  if (ragged) {
+    d_ss = c->span_steps.get<int>(n_spans);
+    if (!d_ss) return fail(UWB_CUDA_ERROR, "device allocation failed");
+    xfer(c, d_ss, span_steps.data(), n_spans * sizeof(int), cudaMemcpyHostToDevice, c->stream);
   }
   const std::vector<double>& ze = stb.zend;
   const std::vector<double>& zm = stb.zmid;
@@ -156,6 +171,7 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   P->half_band = g->half_band;
   P->n_spans = n_spans;
   P->steps = steps;
+  P->span_steps = d_ss;
   P->log2rho = d_tab;
   P->col_stride = NS;
   P->span_stride = cols;
@@ -169,8 +185,7 @@ int upload_path_inputs(uwb_ctx* c, const uwb_grid* g, int n_spans, const uwb_spa
   P->beta2 = beta[0];
   P->beta3 = beta[1];
   P->beta4 = beta[2];
-  c->last_steps = steps;
-  c->last_spans = n_spans;
+  c->last_total_steps = static_cast<double>(total_steps);
   return UWB_OK;
 }
 
@@ -254,7 +269,8 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
   }
   cudaEventRecord(c->ev0, st);
   if (np) {
-    const int per_sm = nli_ctas_per_sm(P.steps, P.n_spans == 1, P.n_r, P.mixed != 0, P.slow_tiny != 0);
+    const int per_sm = nli_ctas_per_sm(P.steps, P.n_spans == 1, P.n_r, P.mixed != 0, P.slow_tiny != 0,
+                                       P.span_steps != nullptr);
     if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
     const int launched = launch_nli(P, F, c->sm_count * per_sm, st, c->evk0, c->evk1);
     if (launched < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
@@ -278,7 +294,7 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
       xfer_sync(c, ne, P.n_eval, sizeof ne, cudaMemcpyDeviceToHost);
       c->last_points = static_cast<double>(ne[0]);
       c->last_active = static_cast<double>(ne[1]);
-      c->last_inner_steps = static_cast<double>(ne[0]) * P.steps * P.n_spans;
+      c->last_inner_steps = static_cast<double>(ne[0]) * c->last_total_steps;
     }
   }
   return UWB_OK;
@@ -382,7 +398,7 @@ void uwb_ctx_destroy(uwb_ctx* c) {
   c->bsubs.clear();
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   for (DBuf* b : {&c->freq, &c->psd, &c->gamma, &c->log2rho, &c->zedge, &c->zstart, &c->zmid, &c->width,
-                  &c->wlast, &c->probe_nu, &c->probe_chan, &c->probe_work, &c->rowcnt, &c->probe_gamma, &c->hl2, &c->rowsum, &c->counter,
+                  &c->wlast, &c->span_steps, &c->probe_nu, &c->probe_chan, &c->probe_work, &c->rowcnt, &c->probe_gamma, &c->hl2, &c->rowsum, &c->counter,
                   &c->n_eval, &c->probe_g, &c->probe_quad, &c->chan_probe0, &c->eta, &c->nli_psd,
                   &c->nli_power, &c->quad, &c->skipped, &c->batch_psd, &c->batch_report, &c->batch_ode, &c->alpha, &c->aeff, &c->raman_x,
                   &c->raman_y, &c->nf_db, &c->guard, &c->rho_end, &c->ode_work, &c->ode_gwork, &c->report,
@@ -554,7 +570,7 @@ int uwb_last_nli_stats(uwb_ctx* c, double* kernel_ms, double* inner_steps,
     if (d_ne) cudaMemcpy(ne, d_ne, sizeof ne, cudaMemcpyDeviceToHost);
     c->last_points = static_cast<double>(ne[0]);
     c->last_active = static_cast<double>(ne[1]);
-    c->last_inner_steps = static_cast<double>(ne[0]) * c->last_steps * c->last_spans;
+    c->last_inner_steps = static_cast<double>(ne[0]) * c->last_total_steps;
   }
   if (kernel_ms) *kernel_ms = c->last_kernel_ms;
   if (inner_steps) *inner_steps = c->last_inner_steps;

@@ -57,7 +57,7 @@ struct uwb_ctx {
   // channel grid
   uwb::DBuf freq, psd, gamma;
   // spans
-  uwb::DBuf log2rho, zedge, zstart, zmid, width, wlast;
+  uwb::DBuf log2rho, zedge, zstart, zmid, width, wlast, span_steps;
   // probes + work
   uwb::DBuf probe_work;  // per-probe |K|^2 evaluations of the last NLI
   uwb::DBuf rowcnt;      // per-row work counts (summed per probe by the finalize)
@@ -80,7 +80,7 @@ struct uwb_ctx {
   unsigned long long h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of the last call
   int last_launches = 0;
   bool nli_events_valid = false;
-  int last_steps = 0, last_spans = 1;  // of the last non-resident NLI upload  // evk0/evk1 bracket the last integrand launch
+  double last_total_steps = 0.0;  // distance steps summed over the spans of the last NLI
   double last_kernel_ms = 0.0;
   double last_inner_steps = 0.0;
   double last_points = 0.0;

@@ -203,7 +203,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   if ((rc = distance_grid_host(fb->length_m, lk->density, &edge, &mid, &width))) return rc;
   const int steps = static_cast<int>(mid.size());
   if (steps > kMaxSteps)
-    return fail(UWB_CONFIG_ERROR, "uwb: distance steps per span must be in [1, 512]");
+    return fail(UWB_CONFIG_ERROR, "uwb: distance steps per span must be in [1, 65536]");
   const int n = g->n_ch;
   std::unique_ptr<uwb_ctx::Prepared> owner(new uwb_ctx::Prepared());
   uwb_ctx::Prepared* pr = owner.get();
@@ -264,8 +264,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   P.beta2 = fb->beta[0];
   P.beta3 = fb->beta[1];
   P.beta4 = fb->beta[2];
-  c->last_steps = steps;
-  c->last_spans = fb->span_count;
+  c->last_total_steps = static_cast<double>(steps) * fb->span_count;
 
   // Probes: every non-guard channel of the subset, lit or dark.  The
   // reference re-derives its skip set (guard or psd <= 0, gn_integral.hpp:
@@ -625,7 +624,7 @@ int uwb_evaluate_link(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
     xfer_sync(c, ne, pr->P.n_eval, sizeof ne, cudaMemcpyDeviceToHost);
     c->last_points = static_cast<double>(ne[0]);
     c->last_active = static_cast<double>(ne[1]);
-    c->last_inner_steps = static_cast<double>(ne[0]) * pr->P.steps * pr->P.n_spans;
+    c->last_inner_steps = static_cast<double>(ne[0]) * c->last_total_steps;
   }
   return UWB_OK;
 }

@@ -626,3 +626,56 @@ def test_long_spans_vs_oracle(density, oracle, engine):
     g2, fibre = product_scenario(case)
     rep = uwb.evaluate_link(fibre, g2, uwb.LinkConfig(gn=cfg_of(case)), engine=engine)
     assert _rel(rep.eta, ref["eta"]) < 1e-8
+
+
+# ---------------------------------------------------------------- spans of their own
+def _span_of(oracle, case):
+    """One span's evolution (its own distance grid) for `case`'s grid."""
+    prep = oracle.prepare(case)
+    return prep, prep["spans"][0]
+
+
+def test_spans_with_different_lengths_and_densities_vs_oracle(oracle, engine):
+    """The reference builds one SpanView per span and walks each span's own
+    step count (gn_integral.hpp:95-99, 141-145, 231-251): an 80 km span at
+    1.4 steps/km (112 steps) followed by a 50 km span at 0.95 steps/km
+    (48 steps) -- previously a ConfigError here -- against the oracle."""
+    a = oband11(n_r=30, density=1.4, length_m=80e3)
+    b = oband11(n_r=30, density=0.95, length_m=50e3)
+    prep, sa = _span_of(oracle, a)
+    _, sb = _span_of(oracle, b)
+    assert sa["steps"] != sb["steps"]
+    prep = dict(prep)
+    prep["spans"] = [sa, sb]
+    ref = oracle.all_channels_nli(a, prep)
+    grid, _, betas, gamma = engine_inputs_from_oracle(dict(prep, spans=[sa]), a.density)
+    spans = []
+    for s in (sa, sb):
+        zg = uwb.DistanceGrid(s["edge"], s["mid"], s["width"], s["length"], 1.0)
+        spans.append(uwb.PowerEvolution(zg, grid.freq, grid.psd * grid.bch, s["log_rho"],
+                                        prep["rho_end"], grid.spacing))
+    r = uwb.all_channels_nli(grid, spans, betas, None, cfg_of(a), engine=engine, gamma=gamma)
+    assert np.array_equal(r.skipped, ref["skipped"])
+    assert _rel(r.eta, ref["eta"]) < NLI_TOL
+    assert _rel(np.asarray(r.quadrant).ravel(), np.asarray(ref["quadrant"]).ravel()) < NLI_TOL
+    # the span order matters (z offsets): swapped spans are a different link
+    ref2 = oracle.all_channels_nli(a, dict(prep, spans=[sb, sa]))
+    r2 = uwb.all_channels_nli(grid, spans[::-1], betas, None, cfg_of(a), engine=engine, gamma=gamma)
+    assert _rel(r2.eta, ref2["eta"]) < NLI_TOL
+
+
+@pytest.mark.parametrize("density", [8.0])
+def test_spans_beyond_512_steps_vs_oracle(density, oracle, engine):
+    """More than 512 distance steps per span (80 km at 8 steps/km = 640
+    steps): the rolled K = 0 integrand, previously a ConfigError, against the
+    oracle; and the full device path (ODE table in the same layout)."""
+    case = oband11(n_r=12, density=density, name=f"long{density}")
+    prep = oracle.prepare(case)
+    assert prep["spans"][0]["steps"] > 512
+    ref = oracle.all_channels_nli(case, prep)
+    grid, spans, betas, gamma = engine_inputs_from_oracle(prep, case.density)
+    r = uwb.all_channels_nli(grid, spans, betas, None, cfg_of(case), engine=engine, gamma=gamma)
+    assert _rel(r.eta, ref["eta"]) < NLI_TOL
+    g2, fibre = product_scenario(case)
+    rep = uwb.evaluate_link(fibre, g2, uwb.LinkConfig(gn=cfg_of(case)), engine=engine)
+    assert _rel(rep.eta, ref["eta"]) < 1e-8
