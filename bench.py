@@ -42,6 +42,12 @@ sys.path.insert(0, ROOT)
 METRIC = "s per full-band SNR eval (589x96GBaud, 80km)"
 UNIT = "s"
 FLOPS_PER_STEP = 87.0  # SURVEY §8(d) frozen convention, FP64 flops per inner phasor step
+# FP64 flops the integrand actually EXECUTES per computed step, from the SASS
+# of its ncu capture (2 DFMA + DADD + DMUL, predicated-on thread instructions
+# over the inner steps; profiles/r02_nli_ncu_summary.txt): the convention
+# above counts the reference's arithmetic, this counts the device's.
+EXECUTED_FLOPS_PER_STEP = 63.04
+FP64_FLOPS_PER_SM_CLK = 128.0  # B200: 64 FP64 FMA per SM per clock
 
 
 def parse():
@@ -473,6 +479,12 @@ def run_engine(args):
         # 1 and 3) share |K|^2 between u2 and -u2, so fewer steps are computed
         effective = FLOPS_PER_STEP * inner_ref / (kmax * 1e-3) / 1e12 / world if kmax > 0 else None
         tr = read_traffic()
+        csum = clk.summary()
+        sm_count = eng.device_info()["sm_count"]
+        max_mhz = csum.get("sm_max_mhz") or 1965.0
+        nominal = sm_count * FP64_FLOPS_PER_SM_CLK * max_mhz * 1e6 / 1e12
+        executed = (EXECUTED_FLOPS_PER_STEP * inner / (kmax * 1e-3) / 1e12 / world
+                    if kmax > 0 else None)
         line = {
             "metric": METRIC, "value": ms_per / 1e3, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per,
@@ -493,9 +505,14 @@ def run_engine(args):
                          "ode_ms": omax,
                          "flops_per_step": FLOPS_PER_STEP,
                          "peak_source": "live DFMA microbenchmark (uwb_fp64_peak), this GPU",
+                         "nominal_peak": nominal,
+                         "frac_vs_nominal": achieved / nominal if achieved else None,
+                         "executed_flops_per_step": EXECUTED_FLOPS_PER_STEP,
+                         "achieved_executed": executed,
+                         "frac_executed": executed / peak if executed else None,
                          "kernel_share_of_step": kmax / ms_per if ms_per else None},
             "cpu_baseline": cpu,
-            "clocks": clk.summary(),
+            "clocks": csum,
             "gpu_launches": int(launches),
             "variants": variants,
             "result_check": {"loss": float(rep[4 * n]), "total_capacity_tbps": float(rep[4 * n + 1]) / 1e12},

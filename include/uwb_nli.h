@@ -277,6 +277,9 @@ int uwb_last_nli_active(uwb_ctx* ctx, double* active_points);
 int uwb_last_ode_stats(uwb_ctx* ctx, double* ode_ms, long long* rhs_evals);
 /* Host<->device bytes moved by the last public call. */
 int uwb_last_transfer_bytes(uwb_ctx* ctx, unsigned long long* h2d, unsigned long long* d2h);
+/* Bounds-checked builds (-DUWB_BOUNDS_CHECK=1): first source line of the
+ * integrand / ODE whose index check failed (0 = none), -1 in normal builds. */
+int uwb_debug_bounds(int* nli_line, int* ode_line);
 /* Live FP64 FMA-pipe peak of this device, TFLOP/s (roofline denominator). */
 int uwb_fp64_peak(uwb_ctx* ctx, double* tflops);
 /* Step arithmetic of the NLI integrand for subsequent calls (and for

@@ -127,6 +127,7 @@ SIGNATURES = {
     "uwb_last_transfer_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_ulonglong),
                                           C.POINTER(C.c_ulonglong)]),
     "uwb_fp64_peak": (C.c_int, [C.c_void_p, DP]),
+    "uwb_debug_bounds": (C.c_int, [IP, IP]),
     "uwb_set_precision": (C.c_int, [C.c_void_p, C.c_int]),
     "uwb_set_ode_stepping": (C.c_int, [C.c_void_p, C.c_int]),
     "uwb_last_launch_count": (C.c_int, [C.c_void_p]),

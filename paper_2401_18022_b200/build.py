@@ -59,15 +59,22 @@ def compile_link(out, extra=(), verbose=False, cache=True):
     from concurrent.futures import ThreadPoolExecutor
 
     os.makedirs(OBJ_DIR, exist_ok=True)
-    tag = hashlib.sha1(" ".join(ARCH + FLAGS + list(extra)).encode()).hexdigest()[:8]
-    objs = [os.path.join(OBJ_DIR, os.path.splitext(src)[0] + "." + tag + ".o") for src in SOURCES]
-    hdr_t = max(os.path.getmtime(h) for h in _headers())
+    # objects are keyed by the CONTENT of the flags, the source and every
+    # header (not by mtimes: an edit during a compile must not leave a stale
+    # object that looks fresh)
+    hh = hashlib.sha1(" ".join(ARCH + FLAGS + list(extra)).encode())
+    for h in sorted(_headers()):
+        hh.update(open(h, "rb").read())
+
+    def key(src):
+        k = hh.copy()
+        k.update(open(os.path.join(CSRC, src), "rb").read())
+        return k.hexdigest()[:12]
+
+    objs = [os.path.join(OBJ_DIR, os.path.splitext(src)[0] + "." + key(src) + ".o") for src in SOURCES]
 
     def stale(src, obj):
-        if not cache or not os.path.exists(obj):
-            return True
-        t = os.path.getmtime(obj)
-        return t < os.path.getmtime(os.path.join(CSRC, src)) or t < hdr_t
+        return not cache or not os.path.exists(obj)
 
     def cc(args):
         src, obj = args

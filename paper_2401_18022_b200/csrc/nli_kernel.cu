@@ -41,6 +41,22 @@ namespace uwb {
 
 namespace {
 
+// Bounds-checked build (-DUWB_BOUNDS_CHECK=1, tools/build_variant.py): every
+// table, record and row index the integrand forms is checked against its
+// allocation; the first failing source line is kept for uwb_debug_bounds.
+// (compute-sanitizer is not available on the GPU pool; this is its stand-in.)
+#if UWB_BOUNDS_CHECK
+__device__ int g_nli_bounds_fail;
+#define UWB_BOUND(cond)                                          \
+  do {                                                           \
+    if (!(cond)) atomicCAS(&g_nli_bounds_fail, 0, __LINE__);     \
+  } while (0)
+#else
+#define UWB_BOUND(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 #ifndef UWB_NLI_WARPS
 #define UWB_NLI_WARPS 8
 #endif
@@ -344,6 +360,10 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
   const double phi = ph.x;
   const double w0 = wa.x, w1 = wa.y, w2 = wb.x, w3 = wb.y, w4 = wc.x, w5 = wc.y;
   const int oa = cl.x + sl, ob = cl.y + sl, oc = cl.z + sl;
+  // columns i0 and i0 + 1 of every stencil inside the [n_ch + 1][NS] table
+  UWB_BOUND(cl.x >= 0 && cl.y >= 0 && cl.z >= 0 && max(cl.x, max(cl.y, cl.z)) + 2 * NS <=
+                                                       (P.n_ch + 1) * NS);
+  UWB_BOUND(idx >= 0 && idx < 32 && probe < P.n_probes);
   double fre = 0.0, fim = 0.0, sre = 0.0, sim = 0.0;
   const int n_spans = HOIST ? 1 : P.n_spans;
   for (int k = 0; k < n_spans; ++k) {
@@ -760,6 +780,8 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
         // Column i0 + 1 is always read: clamped stencils have hw1 = 0 and the
         // table carries a zero pad column n.
         const int pos = fast ? __popc(fm & lt) : __popc(fm) + __popc(sm & lt);
+        UWB_BOUND(pos >= 0 && pos < 32);
+        UWB_BOUND(st1.i1 <= P.n_ch && st2.i1 <= P.n_ch && st3.i1 <= P.n_ch);
         PointRec& R = S.pt[pos];
         R.col[0] = st1.i0 * NS;
         R.col[1] = st2.i0 * NS;
@@ -789,12 +811,14 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
         if (ok && sl == 0) S.kv[S.pt[idx].src] = kv;
       }
       __syncwarp();
+      UWB_BOUND(!valid || (j >= 0 && j < n_r));
       if (valid) val_row[j] = active ? pw * (need ? S.kv[lane] : S.kv[lane ^ 16]) : 0.0;
       __syncwarp();
     }
     if (lane == 0) {
       double acc = 0.0;
       for (int t = 0; t < n_r; ++t) acc += val_row[t];  // ascending j (gn_integral.hpp:288-305)
+      UWB_BOUND(row < P.total_rows);
       P.rowsum[row] = acc * du1 * S.du2;
       P.rowcnt[row] = make_uint2(n_eval, n_act_row);  // summed per probe by the finalize
     }
@@ -1001,6 +1025,16 @@ __global__ void __launch_bounds__(256) dfma_peak_kernel(double* out, int iters, 
 }
 
 }  // namespace
+
+int nli_bounds_status() {
+#if UWB_BOUNDS_CHECK
+  int v = 0;
+  cudaMemcpyFromSymbol(&v, g_nli_bounds_fail, sizeof v);
+  return v;
+#else
+  return -1;  // not a bounds-checked build
+#endif
+}
 
 double fp64_fma_peak_tflops(int sm_count, cudaStream_t st) {
   const int blocks = sm_count * 8, threads = 256, iters = 2048;

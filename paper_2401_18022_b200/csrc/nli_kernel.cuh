@@ -144,6 +144,10 @@ constexpr int kTablePad = 32;
 
 // Live FP64 pipe peak (TFLOP/s): independent DFMA chains on every SM, timed
 // with CUDA events.  The roofline denominator for the integrand kernel.
-double fp64_fma_peak_tflops(int sm_count, cudaStream_t stream);  // 16 lanes x 16 steps per lane
+double fp64_fma_peak_tflops(int sm_count, cudaStream_t stream);
+// First failing line of the bounds-checked build (0: none; -1: not built with
+// -DUWB_BOUNDS_CHECK=1).  Per translation unit: nli_kernel.cu / raman_ode.cu.
+int nli_bounds_status();
+int ode_bounds_status();  // 16 lanes x 16 steps per lane
 
 }  // namespace uwb

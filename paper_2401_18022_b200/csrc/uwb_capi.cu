@@ -612,6 +612,12 @@ int uwb_set_ode_stepping(uwb_ctx* c, int mode) {
   return UWB_OK;
 }
 
+int uwb_debug_bounds(int* nli_line, int* ode_line) {
+  if (nli_line) *nli_line = nli_bounds_status();
+  if (ode_line) *ode_line = ode_bounds_status();
+  return UWB_OK;
+}
+
 int uwb_fp64_peak(uwb_ctx* c, double* tflops) {
   if (!c) return set_err(UWB_CONFIG_ERROR, "null context");
   if (c->multi()) return uwb_fp64_peak(c->subs[0], tflops);
