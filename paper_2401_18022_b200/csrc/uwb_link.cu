@@ -437,15 +437,19 @@ int run_prepared(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_
   return rc;
 }
 
-int check_status(uwb_ctx* c) {
-  int status = 0;
-  xfer_sync(c, &status, c->prep->d_status, sizeof(int), cudaMemcpyDeviceToHost);
+int status_error(int status) {
   switch (status) {
     case 0: return UWB_OK;
     case 1: return fail(UWB_SOLVER_ERROR, "power evolution: non-positive rho");
     case 2: return fail(UWB_SOLVER_ERROR, "rk45: step budget exhausted");
     default: return fail(UWB_SOLVER_ERROR, "rk45: step size underflow");
   }
+}
+
+int check_status(uwb_ctx* c) {
+  int status = 0;
+  xfer_sync(c, &status, c->prep->d_status, sizeof(int), cudaMemcpyDeviceToHost);
+  return status_error(status);
 }
 
 }  // namespace uwb
@@ -591,24 +595,40 @@ int uwb_evaluate_link(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
   if ((rc = run_prepared(c, nullptr, c->stream))) return rc;
   const int n = pr->n;
   cudaStream_t st = c->stream;
-  std::vector<double> rep(4 * static_cast<size_t>(n) + 3 + 2 * pr->L.n_bands);
-  xfer(c, rep.data(), pr->L.out, rep.size() * sizeof(double), cudaMemcpyDeviceToHost, st);
+  // report, status word and work counters land in pinned staging: one
+  // synchronisation for all of them
+  const size_t rl = 4 * static_cast<size_t>(n) + 3 + 2 * pr->L.n_bands;
+  const size_t need = (rl + 4) * sizeof(double);
+  if (c->pinned_cap < need) {
+    if (c->pinned) cudaFreeHost(c->pinned);
+    c->pinned = nullptr;
+    c->pinned_cap = 0;
+    if (cudaMallocHost(&c->pinned, need) != cudaSuccess) return fail(UWB_CUDA_ERROR, "pinned alloc");
+    c->pinned_cap = need;
+  }
+  double* rep = static_cast<double*>(c->pinned);
+  int* status = reinterpret_cast<int*>(rep + rl);
+  unsigned long long* ne = reinterpret_cast<unsigned long long*>(rep + rl + 1);
+  xfer(c, rep, pr->L.out, rl * sizeof(double), cudaMemcpyDeviceToHost, st);
+  xfer(c, status, pr->d_status, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (pr->P.n_probes > 0)
+    xfer(c, ne, pr->P.n_eval, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
   if (out && out->rho_end)
     xfer(c, out->rho_end, pr->O.rho_end, n * sizeof(double), cudaMemcpyDeviceToHost, st);
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "evaluate_link");
-  if ((rc = check_status(c))) return rc;
+  if ((rc = status_error(*status))) return rc;
   if (out) {
-    if (out->eta) std::memcpy(out->eta, rep.data(), n * sizeof(double));
-    if (out->p_ase) std::memcpy(out->p_ase, rep.data() + n, n * sizeof(double));
-    if (out->snr_db) std::memcpy(out->snr_db, rep.data() + 2 * n, n * sizeof(double));
-    if (out->capacity) std::memcpy(out->capacity, rep.data() + 3 * n, n * sizeof(double));
+    if (out->eta) std::memcpy(out->eta, rep, n * sizeof(double));
+    if (out->p_ase) std::memcpy(out->p_ase, rep + n, n * sizeof(double));
+    if (out->snr_db) std::memcpy(out->snr_db, rep + 2 * n, n * sizeof(double));
+    if (out->capacity) std::memcpy(out->capacity, rep + 3 * n, n * sizeof(double));
     out->loss_value = rep[4 * n];
     out->total_capacity = rep[4 * n + 1];
     out->total_power_dbm = rep[4 * n + 2];
     const int nb = pr->L.n_bands;
-    if (out->band_power_dbm) std::memcpy(out->band_power_dbm, rep.data() + 4 * n + 3, nb * 8);
-    if (out->band_capacity) std::memcpy(out->band_capacity, rep.data() + 4 * n + 3 + nb, nb * 8);
+    if (out->band_power_dbm) std::memcpy(out->band_power_dbm, rep + 4 * n + 3, nb * 8);
+    if (out->band_capacity) std::memcpy(out->band_capacity, rep + 4 * n + 3 + nb, nb * 8);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);
     out->elapsed_seconds = ms * 1e-3;
@@ -620,8 +640,6 @@ int uwb_evaluate_link(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
     float kms = 0.f;
     cudaEventElapsedTime(&kms, c->evk0, c->evk1);
     c->last_kernel_ms = kms;
-    unsigned long long ne[2] = {0, 0};
-    xfer_sync(c, ne, pr->P.n_eval, sizeof ne, cudaMemcpyDeviceToHost);
     c->last_points = static_cast<double>(ne[0]);
     c->last_active = static_cast<double>(ne[1]);
     c->last_inner_steps = static_cast<double>(ne[0]) * c->last_total_steps;

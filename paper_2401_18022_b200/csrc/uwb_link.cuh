@@ -71,5 +71,7 @@ int run_report(uwb_ctx* c, cudaStream_t st, const LinkDev* Lp = nullptr);
 int run_prepared(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_status = true);
 // SolverError from the device status word (synchronises the context stream).
 int check_status(uwb_ctx* c);
+// SolverError for a status word already on the host (0 = OK).
+int status_error(int status);
 
 }  // namespace uwb

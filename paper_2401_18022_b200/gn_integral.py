@@ -214,8 +214,26 @@ class FibreSpec:
     raman_y: object = None
 
     def sample(self, freq, lambda_beta):
-        lib = N.load()
+        """Per-channel alpha / A_eff / gamma, the Raman table and beta at
+        lambda_beta, from the engine's host fibre model.  A pure function of
+        the spec and the frequencies: memoised (the optimisation loop and
+        repeated evaluate_link calls sample the same grid)."""
         freq = N.f64(freq)
+        key = (self.length_m, self.span_count, self.flat_alpha_db_km,
+               None if self.raman_x is None else N.f64(self.raman_x).tobytes(),
+               None if self.raman_y is None else N.f64(self.raman_y).tobytes(),
+               float(lambda_beta), freq.tobytes())
+        hit = _SAMPLE_CACHE.get(key)
+        if hit is None:
+            hit = self._sample(freq, lambda_beta)
+            if len(_SAMPLE_CACHE) >= 16:
+                _SAMPLE_CACHE.pop(next(iter(_SAMPLE_CACHE)))
+            _SAMPLE_CACHE[key] = hit
+        # copies: a caller may modify what it gets back
+        return {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in hit.items()}
+
+    def _sample(self, freq, lambda_beta):
+        lib = N.load()
         n = len(freq)
         alpha, aeff, gamma = np.zeros(n), np.zeros(n), np.zeros(n)
         s = N.FibreSample()
@@ -232,6 +250,9 @@ class FibreSpec:
         return dict(alpha=alpha, aeff=aeff, gamma=gamma, beta=np.array(s.beta[:]),
                     raman_x=rx, raman_y=ry,
                     raman_aeff_ref=s.raman_aeff_ref, dispersion=np.array(s.dispersion[:]))
+
+
+_SAMPLE_CACHE: dict = {}
 
 
 def default_fibre() -> FibreSpec:
