@@ -57,6 +57,15 @@ __device__ int g_nli_bounds_fail;
   } while (0)
 #endif
 
+#ifndef UWB_PF
+#define UWB_PF 0
+#endif
+#ifndef UWB_Z_SMEM
+#define UWB_Z_SMEM 0  // HOIST: z edges from shared memory instead of registers
+#endif
+#ifndef UWB_H_SMEM
+#define UWB_H_SMEM 0  // HOIST: probe half-logs from shared memory instead of registers
+#endif
 #ifndef UWB_NLI_WARPS
 #define UWB_NLI_WARPS 8
 #endif
@@ -120,16 +129,20 @@ __device__ __forceinline__ double phase_mismatch(double f1, double f2, double fi
 // One listed point, packed so a 16-lane segment reads it with five broadcast
 // 128-bit loads.
 struct alignas(16) PointRec {
-  double w[6];        // 16 x half weights for columns i0 and i0 + 1 of nu1, nu2, nu3
-  double phi, invphi;  // invphi = 1/phi (0 when phi == 0: no fast span then)
+  double w[6];         // 16 x half weights for columns i0 and i0 + 1 of nu1, nu2, nu3
+  double phi8, rphi8;  // phi 8/pi (the fast branch's phase in units of pi/8) and 1/phi8
+                       // (0 when phi == 0: no fast span then)
   int col[3];          // element offset (i0 * NS) of each stencil's first column
   int src;             // chunk-local column of the listed point
-  double pw;           // p1 * p2 * p3
+  double phi;          // phase mismatch itself (sinc branch, fast/slow test of later spans)
   double pad;
 };
 
 struct WarpSmem {
   PointRec pt[32];
+#if UWB_H_SMEM
+  double h[128];     // the row's probe half-log column (HOIST, K <= 8), lane order
+#endif
   double kv[32];     // |kernel|^2 of each chunk lane's evaluated point
   double nu, f, s1, s2, su, u1, lo, du2;
   int sym;           // row symmetric under u2 -> -u2 (b1 == b2: quadrants 1, 3)
@@ -224,6 +237,59 @@ __constant__ double c_tab_sin16[16] = UWB_SIN_TABLE16;
 // and no second base address)
 __shared__ double2 s_cs16[16];
 
+// The hot loop's shared tables (kernel scope, passed by reference):
+//   cs16[q]: (cos, sin)(q pi/8)
+//   e2c[j]:  2^(j/16) with j << 16 subtracted from its high word, so that adding
+//            k << 16 (k = 16 e + j) to it yields 2^(k/16) exactly: the exponent
+//            insertion is one shift-add (LEA) instead of shift, mask and add.
+struct StepTabs {
+  double2 cs16[16];
+  double e2c[16];
+#if UWB_Z_SMEM
+  double z[128];  // the span's end-edge positions (HOIST, K <= 8), lane order
+#endif
+};
+
+__device__ __forceinline__ double& S_h(WarpSmem& S, int i) {
+#if UWB_H_SMEM
+  return S.h[i];
+#else
+  return S.kv[i & 31];  // not reached
+#endif
+}
+
+template <class T>
+__device__ __forceinline__ double TB_z(const T& tb, int i) {
+#if UWB_Z_SMEM
+  return tb.z[i];
+#else
+  return 0.0;
+#endif
+}
+
+__device__ __forceinline__ void init_step_tabs(StepTabs& T, int i) {
+  if (i < 16) {
+    T.cs16[i] = make_double2(c_tab_cos16[i], c_tab_sin16[i]);
+    const double v = c_exp2_tab16[i];
+    T.e2c[i] = __hiloint2double(__double2hiint(v) - (i << 16), __double2loint(v));
+  }
+}
+
+// 2^(x/16) (uwb_devmath.cuh step_exp2_16; the same value bit for bit: the
+// power-of-two scale is applied to the table entry before the product)
+__device__ __forceinline__ double step_exp2_16t(double x, const StepTabs& T) {
+  const double t = x + kMagic;
+  const int k = __double2loint(t);
+  const double r = x - (t - kMagic);
+  double p = fma(r, c_e4f[3], c_e4f[2]);
+  p = fma(p, r, c_e4f[1]);
+  p = fma(p, r, c_e4f[0]);
+  p = fma(p, r, 1.0);
+  const double v = T.e2c[k & 15];
+  return __hiloint2double(__double2hiint(v) + (k << 16), __double2loint(v)) * p;
+}
+
+
 __device__ __forceinline__ void dev_sincos_table(double x, double* c_out, double* s_out) {
   const double t = fma(x, c_red8[0], kMagic);
   const int q = __double2loint(t) & 15;
@@ -264,6 +330,33 @@ __device__ __forceinline__ void dev_sincos_table(double x, double* c_out, double
 
 __device__ __forceinline__ void dev_sincos(double x, double* c_out, double* s_out) {
   dev_sincos_table(x, c_out, s_out);
+}
+
+// Fast-branch phasor (cos, sin)(phi z) / a, a = pi/8, from phi8 = phi 8/pi
+// (uwb_devmath.cuh step_sincos8): k = rint(phi8 z), r = phi8 z - k by one FMA
+// (|r| <= 1/2, no Cody-Waite constants, no phi z product), kernels with the
+// powers of a folded into their coefficients, the 16-entry (cos, sin)(k pi/8)
+// table.  15 FP64 instructions where dev_sincos(phi z) took 17.
+__constant__ double c_s8[3] = {kStep8S0, kStep8S1, kStep8S2};
+__constant__ double c_c8[4] = {kStep8C0, kStep8C1, kStep8C2, kInvPio8};
+
+__device__ __forceinline__ void step_sincos8(double phi8, double z, const StepTabs& T,
+                                             double* c_out, double* s_out) {
+  const double t = fma(phi8, z, kMagic);
+  const int q = __double2loint(t) & 15;
+  const double kd = t - kMagic;
+  const double r = fma(phi8, z, -kd);
+  const double zz = r * r;
+  double ps = fma(zz, c_s8[2], c_s8[1]);
+  ps = fma(ps, zz, c_s8[0]);
+  const double sr = fma(r * zz, ps, r);
+  double pc = fma(zz, c_c8[2], c_c8[1]);
+  pc = fma(pc, zz, c_c8[0]);
+  const double cr = fma(pc, zz, c_c8[3]);
+  const double2 cs = T.cs16[q];
+  const double tc = cs.x, ts = cs.y;
+  *c_out = fma(tc, cr, -(ts * sr));
+  *s_out = fma(ts, cr, tc * sr);
 }
 
 // ---- compensated-FP32 ("mixed") step arithmetic (GnSolverConfig precision
@@ -338,16 +431,21 @@ __device__ __forceinline__ void mixed_sincos(double x, float* c_out, float* s_ou
 // (p_N = 0): step b adds (p_{b-1} - p_b) E_b of the previous step, the
 // lane's last step pairs with the next lane's first p (one shuffle per point),
 // so each step costs one exp2 and one sincos and nothing crosses lanes inside
-// the step loop.  Slow branch (:176-188) is the direct sinc form.  Lanes with
-// m >= N (only when N < 16 K) mask p to 0 and feed sincos a 0 angle.
+// the step loop.  The phasors are E / a (a = pi/8, step_sincos8); the sum is
+// divided by j phi8 = j phi / a, which restores the scale.  Slow branch
+// (:176-188) is the direct sinc form.  Lanes with m >= N (only when
+// N < 16 K) mask p to 0 and feed sincos z = 0.
 // HOIST: the lane's K end-edge positions Zr and probe half-logs Hr live in
-// registers for the whole row (single span, K <= 8).
+// registers for the whole row (single span, K <= 8); the row setup's fast
+// flag (span 0's test) and z0 == 0 come in as arguments.
 // K = 0: steps per lane known only at run time (spans longer than 512
 // steps): the same code with rolled step loops.
+// Both half-warps always run this together (warp-uniform point loop), so the
+// segment shuffles use the full mask: no run-time convergence checks.
 template <int K, bool FULL, bool HOIST, bool TINY>
 __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSmem& S, int idx,
-                                               int probe, int sl, unsigned segmask,
-                                               const double (&Zr)[K > 0 ? K : 1],
+                                               int probe, int sl, bool fast0, bool z0zero,
+                                               const StepTabs& TB, const double (&Zr)[K > 0 ? K : 1],
                                                const double (&Hr)[K > 0 ? K : 1]) {
   const int Kr = K > 0 ? K : P.col_stride / 16;
   const int NS = 16 * Kr;
@@ -355,9 +453,9 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
   const double2 wa = *reinterpret_cast<const double2*>(&R.w[0]);
   const double2 wb = *reinterpret_cast<const double2*>(&R.w[2]);
   const double2 wc = *reinterpret_cast<const double2*>(&R.w[4]);
-  const double2 ph = *reinterpret_cast<const double2*>(&R.phi);
+  const double2 ph = *reinterpret_cast<const double2*>(&R.phi8);
   const int4 cl = *reinterpret_cast<const int4*>(&R.col[0]);
-  const double phi = ph.x;
+  const double phi8 = ph.x;
   const double w0 = wa.x, w1 = wa.y, w2 = wb.x, w3 = wb.y, w4 = wc.x, w5 = wc.y;
   const int oa = cl.x + sl, ob = cl.y + sl, oc = cl.z + sl;
   // columns i0 and i0 + 1 of every stencil inside the [n_ch + 1][NS] table
@@ -374,30 +472,58 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
     const double* cb = T + ob;
     const double* cc3 = T + oc;
     const double* hl = P.hl2 + (static_cast<size_t>(probe) * P.n_spans + k) * NS + sl;
-    const bool fast = fabs(phi) * __ldg(P.wlast + k) > 1e-4;
+    const bool fast = HOIST ? fast0 : fabs(R.phi) * __ldg(P.wlast + k) > 1e-4;
+    double p0 = 0.0, pp = 0.0, pc = 0.0, ps = 0.0;
     if (fast) {
       const double* ze = P.zedge + static_cast<size_t>(k) * NS + sl;
-      double p0 = 0.0, pp = 0.0, pc = 0.0, ps = 0.0;
+      // table values of step b + PF are loaded while step b computes
+      // (explicit software pipeline; PF = 0: loads at their use)
+      constexpr int PF = K > 0 ? UWB_PF : 0;
+      double tv[PF + 1][6];
+#pragma unroll
+      for (int d = 0; d < PF; ++d) {
+        const int o = 16 * d;
+        tv[d][0] = __ldg(ca + o), tv[d][1] = __ldg(ca + NS + o);
+        tv[d][2] = __ldg(cb + o), tv[d][3] = __ldg(cb + NS + o);
+        tv[d][4] = __ldg(cc3 + o), tv[d][5] = __ldg(cc3 + NS + o);
+      }
 #pragma unroll(K > 0 ? K : 4)
       for (int b = 0; b < Kr; ++b) {
         const int o = 16 * b;
-        const double H = HOIST ? Hr[b] : __ldg(hl + o);
-        const double Z = HOIST ? Zr[b] : __ldg(ze + o);
-        double lg = fma(w0, __ldg(ca + o), -H);
-        lg = fma(w1, __ldg(ca + NS + o), lg);
-        lg = fma(w2, __ldg(cb + o), lg);
-        lg = fma(w3, __ldg(cb + NS + o), lg);
-        lg = fma(w4, __ldg(cc3 + o), lg);
-        lg = fma(w5, __ldg(cc3 + NS + o), lg);
-        double p = step_exp2_16(lg);
-        double ang = phi * Z;
+        const double H = HOIST ? (UWB_H_SMEM ? S_h(const_cast<WarpSmem&>(S), o + sl) : Hr[b]) : __ldg(hl + o);
+        double Z = HOIST ? (UWB_Z_SMEM ? TB_z(TB, o + sl) : Zr[b]) : __ldg(ze + o);
+        double lg;
+        if constexpr (PF > 0) {
+          if (b + PF < Kr) {
+            const int on = o + 16 * PF;
+            double* t = tv[(b + PF) % (PF + 1)];
+            t[0] = __ldg(ca + on), t[1] = __ldg(ca + NS + on);
+            t[2] = __ldg(cb + on), t[3] = __ldg(cb + NS + on);
+            t[4] = __ldg(cc3 + on), t[5] = __ldg(cc3 + NS + on);
+          }
+          const double* c = tv[b % (PF + 1)];
+          lg = fma(w0, c[0], -H);
+          lg = fma(w1, c[1], lg);
+          lg = fma(w2, c[2], lg);
+          lg = fma(w3, c[3], lg);
+          lg = fma(w4, c[4], lg);
+          lg = fma(w5, c[5], lg);
+        } else {
+          lg = fma(w0, __ldg(ca + o), -H);
+          lg = fma(w1, __ldg(ca + NS + o), lg);
+          lg = fma(w2, __ldg(cb + o), lg);
+          lg = fma(w3, __ldg(cb + NS + o), lg);
+          lg = fma(w4, __ldg(cc3 + o), lg);
+          lg = fma(w5, __ldg(cc3 + NS + o), lg);
+        }
+        double p = step_exp2_16t(lg, TB);
         if (!FULL) {
           const bool ok = sl * Kr + b < N;
           p = ok ? p : 0.0;
-          ang = ok ? ang : 0.0;
+          Z = ok ? Z : 0.0;
         }
         double cs, sn;
-        dev_sincos(ang, &cs, &sn);
+        step_sincos8(phi8, Z, TB, &cs, &sn);
         if (b == 0) {
           p0 = p;
         } else {  // (p_{m-1} - p_m) E_m, E_m = end edge of the previous step
@@ -409,25 +535,8 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
         pc = cs;
         ps = sn;
       }
-      // the lane's last step pairs with the next lane's first (p_N = 0)
-      double pn = __shfl_down_sync(segmask, p0, 1, 16);
-      if (sl == 15) pn = 0.0;
-      const double cf = pp - pn;
-      fre = fma(cf, pc, fre);
-      fim = fma(cf, ps, fim);
-      // -p_0 E(z_0): E = 1 when the span starts at z = 0
-      const double z0 = __ldg(P.zstart + k);
-      if (z0 == 0.0) {
-        if (sl == 0) fre -= p0;
-      } else {
-        double c0v, s0v;
-        dev_sincos(phi * z0, &c0v, &s0v);
-        if (sl == 0) {
-          fre = fma(-p0, c0v, fre);
-          fim = fma(-p0, s0v, fim);
-        }
-      }
     } else {
+      const double phi = R.phi;
       const double* zm = P.zmid + static_cast<size_t>(k) * NS + sl;
       const double* wd = P.width + static_cast<size_t>(k) * NS + sl;
       // fully unrolled like the fast loop (independent steps interleave);
@@ -441,14 +550,14 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
 #pragma unroll(K > 0 ? K : 4)
       for (int b = 0; b < Kr; ++b) {
         const int o = 16 * b;
-        const double H = HOIST ? Hr[b] : __ldg(hl + o);
+        const double H = HOIST ? (UWB_H_SMEM ? S_h(const_cast<WarpSmem&>(S), o + sl) : Hr[b]) : __ldg(hl + o);
         double lg = fma(w0, __ldg(ca + o), -H);
         lg = fma(w1, __ldg(ca + NS + o), lg);
         lg = fma(w2, __ldg(cb + o), lg);
         lg = fma(w3, __ldg(cb + NS + o), lg);
         lg = fma(w4, __ldg(cc3 + o), lg);
         lg = fma(w5, __ldg(cc3 + NS + o), lg);
-        const double p = step_exp2_16(lg);
+        const double p = step_exp2_16t(lg, TB);
         const double wm = __ldg(wd + o);
         // sinc(x), |x| = |phi| w / 2 <= 5e-5 here: 1 - x^2/6 + x^4/120 is exact
         const double x = 0.5 * phi * wm;
@@ -469,15 +578,36 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
         sim = fma(w, sn, sim);
       }
     }
+    // the lane's last step pairs with the next lane's first (p_N = 0); both
+    // half-warps reach this shuffle whatever their branch
+    double pn = __shfl_down_sync(kFull, p0, 1, 16);
+    if (fast) {
+      if (sl == 15) pn = 0.0;
+      const double cf = pp - pn;
+      fre = fma(cf, pc, fre);
+      fim = fma(cf, ps, fim);
+      // -p_0 E(z_0) / a: E = 1 when the span starts at z = 0
+      if (HOIST ? z0zero : __ldg(P.zstart + k) == 0.0) {
+        if (sl == 0) fre = fma(-p0, kInvPio8, fre);
+      } else {
+        double c0v, s0v;
+        step_sincos8(phi8, __ldg(P.zstart + k), TB, &c0v, &s0v);
+        if (sl == 0) {
+          fre = fma(-p0, c0v, fre);
+          fim = fma(-p0, s0v, fim);
+        }
+      }
+    }
   }
-  // fast spans contribute (sum / (j phi)) (gn_integral.hpp:173-175)
-  const double invphi = ph.y;
-  double re = fma(fim, invphi, sre);
-  double im = fma(-fre, invphi, sim);
+  // fast spans contribute (sum / (j phi)) = (scaled sum / (j phi8))
+  // (gn_integral.hpp:173-175)
+  const double rphi8 = ph.y;
+  double re = fma(fim, rphi8, sre);
+  double im = fma(-fre, rphi8, sim);
 #pragma unroll
   for (int o = 8; o >= 1; o >>= 1) {
-    re += __shfl_xor_sync(segmask, re, o, 16);
-    im += __shfl_xor_sync(segmask, im, o, 16);
+    re += __shfl_xor_sync(kFull, re, o, 16);
+    im += __shfl_xor_sync(kFull, im, o, 16);
   }
   return re * re + im * im;
 }
@@ -487,16 +617,15 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
 // FP32, everything across lanes in FP64.
 template <int K, bool FULL, bool HOIST>
 __device__ __forceinline__ double point_kernel_mixed(const NliParams& P, const WarpSmem& S, int idx,
-                                                     int probe, int sl, unsigned segmask,
+                                                     int probe, int sl,
                                                      const double (&Zr)[K], const double (&Hr)[K]) {
   constexpr int NS = 16 * K;
   const PointRec& R = S.pt[idx];
   const double2 wa = *reinterpret_cast<const double2*>(&R.w[0]);
   const double2 wb = *reinterpret_cast<const double2*>(&R.w[2]);
   const double2 wc = *reinterpret_cast<const double2*>(&R.w[4]);
-  const double2 ph = *reinterpret_cast<const double2*>(&R.phi);
   const int4 cl = *reinterpret_cast<const int4*>(&R.col[0]);
-  const double phi = ph.x;
+  const double phi = R.phi;
   const double w0 = wa.x, w1 = wa.y, w2 = wb.x, w3 = wb.y, w4 = wc.x, w5 = wc.y;
   const int oa = cl.x + sl, ob = cl.y + sl, oc = cl.z + sl;
   double fre = 0.0, fim = 0.0, sre = 0.0, sim = 0.0;
@@ -509,11 +638,11 @@ __device__ __forceinline__ double point_kernel_mixed(const NliParams& P, const W
     const double* cc3 = T + oc;
     const double* hl = P.hl2 + (static_cast<size_t>(probe) * P.n_spans + k) * NS + sl;
     const bool fast = fabs(phi) * __ldg(P.wlast + k) > 1e-4;
+    float lre = 0.0f, lim = 0.0f;  // fast branch: the lane's FP32 partial sums
+    float p0 = 0.0f, pp = 0.0f, pc = 0.0f, ps = 0.0f;
+    double lg0 = 0.0, lgp = 0.0;
     if (fast) {
       const double* ze = P.zedge + static_cast<size_t>(k) * NS + sl;
-      float lre = 0.0f, lim = 0.0f;
-      float p0 = 0.0f, pp = 0.0f, pc = 0.0f, ps = 0.0f;
-      double lg0 = 0.0, lgp = 0.0;
 #pragma unroll
       for (int b = 0; b < K; ++b) {
         const int o = 16 * b;
@@ -548,31 +677,10 @@ __device__ __forceinline__ double point_kernel_mixed(const NliParams& P, const W
         pc = cs;
         ps = sn;
       }
-      // the lane's last step pairs with the next lane's first (p_N = 0)
-      float pn = __shfl_down_sync(segmask, p0, 1, 16);
-      const double lgn = __shfl_down_sync(segmask, lg0, 1, 16);
-      if (sl == 15) pn = 0.0f;
-      const float cf = pn == 0.0f ? pp : mixed_dp(pn, pp, __double2float_rn(lgp - lgn));
-      lre = fmaf(cf, pc, lre);
-      lim = fmaf(cf, ps, lim);
-      fre += static_cast<double>(lre);
-      fim += static_cast<double>(lim);
-      // -p_0 E(z_0): E = 1 when the span starts at z = 0
-      const double z0 = __ldg(P.zstart + k);
-      if (z0 == 0.0) {
-        if (sl == 0) fre -= p0;
-      } else {
-        double c0v, s0v;
-        dev_sincos(phi * z0, &c0v, &s0v);
-        if (sl == 0) {
-          fre = fma(-static_cast<double>(p0), c0v, fre);
-          fim = fma(-static_cast<double>(p0), s0v, fim);
-        }
-      }
     } else {
       const double* zm = P.zmid + static_cast<size_t>(k) * NS + sl;
       const double* wd = P.width + static_cast<size_t>(k) * NS + sl;
-      float lre = 0.0f, lim = 0.0f;
+      float ure = 0.0f, uim = 0.0f;
       const float phf = static_cast<float>(phi);
 #pragma unroll
       for (int b = 0; b < K; ++b) {
@@ -593,20 +701,45 @@ __device__ __forceinline__ double point_kernel_mixed(const NliParams& P, const W
         if (!FULL) w = (sl * K + b < N) ? w : 0.0f;
         float cs, sn;
         mixed_sincos(phi * __ldg(zm + o), &cs, &sn);
-        lre = fmaf(w, cs, lre);
-        lim = fmaf(w, sn, lim);
+        ure = fmaf(w, cs, ure);
+        uim = fmaf(w, sn, uim);
       }
-      sre += static_cast<double>(lre);
-      sim += static_cast<double>(lim);
+      sre += static_cast<double>(ure);
+      sim += static_cast<double>(uim);
+    }
+    // the lane's last step pairs with the next lane's first (p_N = 0); both
+    // half-warps reach these shuffles whatever their branch
+    float pn = __shfl_down_sync(kFull, p0, 1, 16);
+    const double lgn = __shfl_down_sync(kFull, lg0, 1, 16);
+    if (fast) {
+      if (sl == 15) pn = 0.0f;
+      const float cf = pn == 0.0f ? pp : mixed_dp(pn, pp, __double2float_rn(lgp - lgn));
+      lre = fmaf(cf, pc, lre);
+      lim = fmaf(cf, ps, lim);
+      fre += static_cast<double>(lre);
+      fim += static_cast<double>(lim);
+      // -p_0 E(z_0): E = 1 when the span starts at z = 0
+      const double z0 = __ldg(P.zstart + k);
+      if (z0 == 0.0) {
+        if (sl == 0) fre -= p0;
+      } else {
+        double c0v, s0v;
+        dev_sincos(phi * z0, &c0v, &s0v);
+        if (sl == 0) {
+          fre = fma(-static_cast<double>(p0), c0v, fre);
+          fim = fma(-static_cast<double>(p0), s0v, fim);
+        }
+      }
     }
   }
-  const double invphi = ph.y;
+  // 1/phi = (8/pi) / phi8 = (8/pi) rphi8
+  const double invphi = R.rphi8 * kInvPio8;
   double re = fma(fim, invphi, sre);
   double im = fma(-fre, invphi, sim);
 #pragma unroll
   for (int o = 8; o >= 1; o >>= 1) {
-    re += __shfl_xor_sync(segmask, re, o, 16);
-    im += __shfl_xor_sync(segmask, im, o, 16);
+    re += __shfl_xor_sync(kFull, re, o, 16);
+    im += __shfl_xor_sync(kFull, im, o, 16);
   }
   return re * re + im * im;
 }
@@ -615,7 +748,8 @@ template <int K, bool FULL, bool HOIST, bool MIXED, bool TINY>
 __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS : UWB_NLI_MIN_BLOCKS)
     nli_rows_kernel(const NliParams P) {
   __shared__ WarpSmem s_w[kWarps];
-  extern __shared__ double row_vals[];  // [kWarps][n_r]
+  __shared__ StepTabs s_tabs;
+  init_step_tabs(s_tabs, threadIdx.x);
   if (threadIdx.x < 16) {
     s_exp2_tab[threadIdx.x] = c_exp2_tab16[threadIdx.x];
     s_cs16[threadIdx.x] = make_double2(c_tab_cos16[threadIdx.x], c_tab_sin16[threadIdx.x]);
@@ -625,6 +759,9 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
       s_sin16f[threadIdx.x] = __double2float_rn(c_tab_sin16[threadIdx.x]);
     }
   }
+#if UWB_Z_SMEM
+  if (HOIST && threadIdx.x < 16 * K) s_tabs.z[threadIdx.x] = __ldg(P.zedge + threadIdx.x);
+#endif
   __syncthreads();
 
   const int NS = 16 * (K > 0 ? K : P.col_stride / 16);
@@ -632,15 +769,16 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
   const int warp = threadIdx.x >> 5;
   const int sl = lane & 15;
   const int seg = lane >> 4;
-  const unsigned segmask = 0xffffu << (16 * seg);
   WarpSmem& S = s_w[warp];
   const int per_probe = P.n_q * P.n_r;
   double Zr[K > 0 ? K : 1], Hr[K > 0 ? K : 1];
   int cur_probe = -1;
-  if (HOIST) {
+  if (HOIST && !UWB_Z_SMEM) {
 #pragma unroll
     for (int b = 0; b < K; ++b) Zr[b] = __ldg(P.zedge + 16 * b + sl);
   }
+  // single span (HOIST): its start z, zero for every grid build_distance_grid makes
+  const bool z0zero = !HOIST || __ldg(P.zstart) == 0.0;
 
   for (;;) {
     int row = 0;
@@ -660,7 +798,14 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
     if (HOIST && probe != cur_probe) {
       cur_probe = probe;
 #pragma unroll
-      for (int b = 0; b < K; ++b) Hr[b] = __ldg(P.hl2 + static_cast<size_t>(probe) * NS + 16 * b + sl);
+      for (int b = 0; b < K; ++b) {
+        const double hv = __ldg(P.hl2 + static_cast<size_t>(probe) * NS + 16 * b + sl);
+        if (UWB_H_SMEM && !MIXED)
+          S_h(S, 16 * b + sl) = hv;  // both half-warps store the same value
+        else
+          Hr[b] = hv;
+      }
+      if (UWB_H_SMEM) __syncwarp();
     }
     const int n_r = P.n_r;
     double du1;
@@ -725,7 +870,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
       __syncwarp();
     }
     unsigned n_eval = 0, n_act_row = 0;
-    double* val_row = row_vals + static_cast<size_t>(warp) * n_r;  // pw |K|^2 per column j
+    double row_acc = 0.0;
     // Symmetric rows (quadrants 1 and 3: s1 == s2, b1 == b2): u2 -> -u2 swaps f1 and f2,
     // and the integrand is symmetric in them (phase_mismatch is bit-exactly
     // symmetric, gn_integral.hpp:43-50; the power factor is a product over
@@ -790,12 +935,14 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
         R.w[0] = st1.hw0 * 16.0; R.w[1] = st1.hw1 * 16.0;
         R.w[2] = st2.hw0 * 16.0; R.w[3] = st2.hw1 * 16.0;
         R.w[4] = st3.hw0 * 16.0; R.w[5] = st3.hw1 * 16.0;
+        const double phi8 = phi * kInvPio8;
+        R.phi8 = phi8;
+        R.rphi8 = phi != 0.0 ? __drcp_rn(phi8) : 0.0;
         R.phi = phi;
-        R.invphi = phi != 0.0 ? __drcp_rn(phi) : 0.0;
-        R.pw = pw;
       }
       __syncwarp();
       const int n_need = __popc(nm);
+      const int n_fast = __popc(fm);
       n_eval += n_need;
       n_act_row += __popc(am);
       // warp-uniform trip count: with an odd count the idle half-warp repeats
@@ -805,21 +952,31 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
         const int idx = ok ? base + seg : base;
         double kv;
         if constexpr (MIXED)
-          kv = point_kernel_mixed<K, FULL, HOIST>(P, S, idx, probe, sl, segmask, Zr, Hr);
+          kv = point_kernel_mixed<K, FULL, HOIST>(P, S, idx, probe, sl, Zr, Hr);
         else
-          kv = point_kernel<K, FULL, HOIST, TINY>(P, S, idx, probe, sl, segmask, Zr, Hr);
+          kv = point_kernel<K, FULL, HOIST, TINY>(P, S, idx, probe, sl, idx < n_fast, z0zero,
+                                                  s_tabs, Zr, Hr);
         if (ok && sl == 0) S.kv[S.pt[idx].src] = kv;
       }
       __syncwarp();
       UWB_BOUND(!valid || (j >= 0 && j < n_r));
-      if (valid) val_row[j] = active ? pw * (need ? S.kv[lane] : S.kv[lane ^ 16]) : 0.0;
+      // row sum (gn_integral.hpp:288-305): each chunk's 32 column values by a
+      // fixed xor tree, chunks added in ascending order -- the order depends
+      // on (n_r, row symmetry) only, so rows are reproducible and independent of
+      // scheduling and partitioning, and no per-row array is kept
+      double v = (valid && active) ? pw * (need ? S.kv[lane] : S.kv[lane ^ 16]) : 0.0;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+      row_acc += v;
       __syncwarp();
     }
+    // row sum (gn_integral.hpp:288-305): lane l adds the contiguous run of
+    // columns [l c, (l + 1) c) in ascending j, then a fixed xor tree; the
+    // order depends on (n_r) only, so rows are reproducible and independent
+    // of scheduling and partitioning
     if (lane == 0) {
-      double acc = 0.0;
-      for (int t = 0; t < n_r; ++t) acc += val_row[t];  // ascending j (gn_integral.hpp:288-305)
       UWB_BOUND(row < P.total_rows);
-      P.rowsum[row] = acc * du1 * S.du2;
+      P.rowsum[row] = row_acc * du1 * S.du2;
       P.rowcnt[row] = make_uint2(n_eval, n_act_row);  // summed per probe by the finalize
     }
     __syncwarp();
@@ -1066,33 +1223,42 @@ int launch_finalize_channels_only(const FinalizeParams& f, cudaStream_t st) {
 }
 
 namespace {
-size_t row_smem(int n_r) { return static_cast<size_t>(kWarps) * n_r * sizeof(double); }
-// static WarpSmem + dynamic row arrays may pass the 48 KB default: raise the
-// kernel's dynamic limit once per (kernel, size) high-water mark
-void allow_row_smem(RowKernel k, int n_r) {
+size_t row_smem(int) { return 0; }  // rows keep no per-column array (running chunk sums)
+// Shared-memory carveout: the smallest configuration that holds the CTAs one
+// SM runs (launch bounds), so the rest of the 256 KB stays L1 for the log2 rho
+// table (the default picked a 132 KB carveout for 2 x 38 KB: 124 KB of L1).
+void allow_row_smem(RowKernel k, int /*n_r*/) {
   // The attribute is per (device, kernel); contexts on several devices are
   // driven from concurrent host threads (optimise_launch_powers), hence the lock.
   struct Seen {
     int dev;
     RowKernel k;
-    size_t b;
   };
   static std::mutex mu;
-  static Seen seen[128];
+  static Seen seen[256];
   static int n_seen = 0;
   int dev = 0;
   cudaGetDevice(&dev);
-  const size_t b = row_smem(n_r);
   std::lock_guard<std::mutex> lock(mu);
   for (int i = 0; i < n_seen; ++i)
-    if (seen[i].dev == dev && seen[i].k == k) {
-      if (seen[i].b >= b) return;
-      seen[i].b = b;
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b));
-      return;
-    }
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b));
-  if (n_seen < 128) seen[n_seen++] = Seen{dev, k, b};
+    if (seen[i].dev == dev && seen[i].k == k) return;
+  static const bool no_carveout = [] {  // UWB_NLI_NO_CARVEOUT=1: driver default (A/B)
+    const char* e = std::getenv("UWB_NLI_NO_CARVEOUT");
+    return e && e[0] == '1';
+  }();
+  cudaFuncAttributes fa{};
+  int per_sm = 0;
+  if (!no_carveout && cudaFuncGetAttributes(&fa, k) == cudaSuccess &&
+      cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) ==
+          cudaSuccess &&
+      per_sm > 0) {
+    // CTAs the register file holds (the launch bounds' target)
+    const int ctas = std::max(1, 65536 / (std::max(fa.numRegs, 1) * kWarps * 32));
+    const size_t need = static_cast<size_t>(ctas) * (fa.sharedSizeBytes + 1024);
+    const int pct = static_cast<int>(std::min<size_t>(100, (100 * need + per_sm - 1) / per_sm));
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  }
+  if (n_seen < 256) seen[n_seen++] = Seen{dev, k};
 }
 }  // namespace
 

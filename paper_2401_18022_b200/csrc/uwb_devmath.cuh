@@ -321,6 +321,44 @@ constexpr double kStepC0 = -0.4999999999556206;
 constexpr double kStepC1 = 0.04166664594464585;
 constexpr double kStepC2 = -0.0013874553368951438;
 
+// The fast branch's sincos works in units of pi/8: with phi8 = phi 8/pi per
+// point, x = phi z = (pi/8)(k + r) where k = rint(phi8 z) and r = phi8 z - k
+// by one FMA (|r| <= 1/2), so the Cody-Waite reduction and the phi z product
+// drop out.  The kernels return cos / sin (a r) divided by a = pi/8, i.e. the
+// phasor scaled by 8/pi; the integrand folds the scale back in through
+// 1/phi8 = (pi/8)/phi.  Coefficients: the kStepS* / kStepC* fits above with
+// the powers of a folded in (50-digit arithmetic, tools/README.md):
+//   sin(a r)/a = r + r^3 (a^2 S0 + r^2 (a^4 S1 + r^2 a^6 S2))
+//   cos(a r)/a = 1/a + r^2 (a C0 + r^2 (a^3 C1 + r^2 a^5 C2))
+// Equivalent to evaluating at phi' = phi8 pi/8 = phi (1 + d), |d| <= 2^-52:
+// a phase error |d phi z| of the same size as the reference's own rounding of
+// phi * (z_base + edge) (gn_integral.hpp:165).
+constexpr double kStep8S0 = -0.02570209479374301;
+constexpr double kStep8S1 = 0.00019817924828540812;
+constexpr double kStep8S2 = -7.270762510593567e-07;
+constexpr double kStep8C0 = -0.19634954083193434;
+constexpr double kStep8C1 = 0.0025232960009761362;
+constexpr double kStep8C2 = -1.2957417140207165e-05;
+constexpr double kInvPio8 = 2.5464790894703255;  // RN(8/pi) = 1/a
+
+// nli_kernel.cu step_sincos8 (same operation sequence): (cos, sin)(phi z) / a.
+UWB_HD void step_sincos8(double phi8, double z, const double* cos16, const double* sin16,
+                         double* c_out, double* s_out) {
+  const double t = fmad(phi8, z, kMagic);
+  const int q = lo_word(t) & 15;
+  const double kd = t - kMagic;
+  const double r = fmad(phi8, z, -kd);
+  const double zz = r * r;
+  double ps = fmad(zz, kStep8S2, kStep8S1);
+  ps = fmad(ps, zz, kStep8S0);
+  const double sr = fmad(r * zz, ps, r);
+  double pc = fmad(zz, kStep8C2, kStep8C1);
+  pc = fmad(pc, zz, kStep8C0);
+  const double cr = fmad(pc, zz, kInvPio8);
+  *c_out = fmad(cos16[q], cr, -(sin16[q] * sr));
+  *s_out = fmad(sin16[q], cr, cos16[q] * sr);
+}
+
 // nli_kernel.cu step_exp2_16 (same operation sequence).
 UWB_HD double step_exp2_16(double x, const double* tab16) {
   const double t = x + kMagic;

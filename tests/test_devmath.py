@@ -3,7 +3,8 @@
 csrc/uwb_devmath.cuh holds __host__ __device__ restatements of the device
 code: the ulp-accurate kernels of the row setup (exp2_16, sincos_tab16) and
 the SHORTER step kernels the hot loop actually runs at UWB_FAST_POLY=2
-(step_exp2_16, step_sincos_tab16: 2^x quartic, sin degree 7, cos degree 6),
+(step_exp2_16: 2^x quartic; step_sincos8, the fast branch's phasor in units
+of pi/8; step_sincos_tab16, the sinc branch's: sin degree 7, cos degree 6),
 whose coefficients nli_kernel.cu's __constant__ banks are initialised from
 (checked below).  Their documented error bounds are asserted here; the GPU
 parity tests cover the kernels end to end."""
@@ -39,6 +40,17 @@ double err_step_exp2_16(const double* x, long n) { long double m = 0; for (long 
 double err_step_sincos16(const double* x, long n, int which) { long double m = 0; for (long i = 0; i < n; ++i) {
   double c, s; uwb::step_sincos_tab16(x[i], C16, S16, &c, &s); long double ec = fabsl(c - cosl((long double)x[i])), es = fabsl(s - sinl((long double)x[i]));
   long double e = which == 0 ? ec : es; if (e > m) m = e; } return (double)m; }
+double err_step_sincos8(const double* phi8, const double* z, long n, int which) { long double m = 0;
+  const long double a = 3.14159265358979323846264338327950288L / 8; for (long i = 0; i < n; ++i) {
+  double c, s; uwb::step_sincos8(phi8[i], z[i], C16, S16, &c, &s);
+  // the kernel evaluates at phi' = phi8 pi/8 exactly and returns the phasor / a; the
+  // reference phase is reduced exactly: phi8 z = k + r (r by a long double FMA),
+  // x = a ((k mod 16) + r) differs from a phi8 z by a multiple of 2 pi
+  const double k = rint(phi8[i] * z[i]);
+  const long double r = fmal((long double)phi8[i], (long double)z[i], -(long double)k);
+  long double x = a * ((long double)fmod(k, 16.0) + r);
+  long double ec = fabsl(c * a - cosl(x)), es = fabsl(s * a - sinl(x));
+  long double e = which == 0 ? ec : es; if (e > m) m = e; } return (double)m; }
 double err_sincos(const double* x, long n) { long double m = 0; for (long i = 0; i < n; ++i) {
   double c, s; uwb::sincos_rd(x[i], &c, &s); long double ec = fabsl(c - cosl((long double)x[i])), es = fabsl(s - sinl((long double)x[i]));
   if (ec > m) m = ec; if (es > m) m = es; } return (double)m; }
@@ -61,6 +73,7 @@ def lib(tmp_path_factory):
     L.err_sincos16.restype = ctypes.c_double
     L.err_step_exp2_16.restype = ctypes.c_double
     L.err_step_sincos16.restype = ctypes.c_double
+    L.err_step_sincos8.restype = ctypes.c_double
     return L
 
 
@@ -124,6 +137,37 @@ def test_step_sincos_error_bounds(lib, scale):
     ec = lib.err_step_sincos16(_p(x), len(x), 0)
     es = lib.err_step_sincos16(_p(x), len(x), 1)
     assert 1e-13 < ec < 1.75e-12 and 1e-13 < es < 1.75e-12, (ec, es)
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e3, 1e5, 3e7])
+def test_step_sincos8_error_bounds(lib, scale):
+    """The fast branch's phasor (step_sincos8): phase phi8 z in
+    units of pi/8 reduced by one FMA, kernels with the powers of pi/8 folded in,
+    result scaled by 8/pi.  Against long double at the exactly represented phase
+    (pi/8) phi8 z: cos and sin each within 1.75e-12 absolute (the fits' own
+    bounds, as for step_sincos_tab16), and a real truncation (> 1e-13)."""
+    rng = np.random.default_rng(7)
+    z = rng.uniform(0.0, 2e5, 300000)
+    phi8 = rng.uniform(-1.0, 1.0, len(z)) * scale / 2e5 * 8 / np.pi
+    ec = lib.err_step_sincos8(_p(phi8), _p(z), len(z), 0)
+    es = lib.err_step_sincos8(_p(phi8), _p(z), len(z), 1)
+    assert 1e-13 < ec < 1.75e-12 and 1e-13 < es < 1.75e-12, (ec, es)
+
+
+def test_step_sincos8_coefficients_are_the_scaled_fits():
+    """kStep8* = kStep* with the powers of a = pi/8 folded in (to 1 ulp)."""
+    import re
+    src = open(os.path.join(ROOT, "paper_2401_18022_b200", "csrc", "uwb_devmath.cuh")).read()
+    c = {m.group(1): float(m.group(2)) for m in
+         re.finditer(r"constexpr double (k\w+) = ([-0-9.e+]+);", src)}
+    a = np.pi / 8
+    for k in range(3):
+        assert c[f"kStep8S{k}"] == pytest.approx(c[f"kStepS{k}"] * a ** (2 * k + 2), rel=4e-16)
+        assert c[f"kStep8C{k}"] == pytest.approx(c[f"kStepC{k}"] * a ** (2 * k + 1), rel=4e-16)
+    assert c["kInvPio8"] == 8 / np.pi
+    dev = open(os.path.join(ROOT, "paper_2401_18022_b200", "csrc", "nli_kernel.cu")).read()
+    assert "c_s8[3] = {kStep8S0, kStep8S1, kStep8S2}" in dev
+    assert "c_c8[4] = {kStep8C0, kStep8C1, kStep8C2, kInvPio8}" in dev
 
 
 def test_step_kernel_coefficients_are_the_device_ones():
