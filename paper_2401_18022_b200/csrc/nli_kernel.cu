@@ -57,17 +57,14 @@ __device__ int g_nli_bounds_fail;
   } while (0)
 #endif
 
-#ifndef UWB_PF
-#define UWB_PF 0
-#endif
 #ifndef UWB_Z_SMEM
-#define UWB_Z_SMEM 0  // HOIST: z edges from shared memory instead of registers
-#endif
-#ifndef UWB_H_SMEM
-#define UWB_H_SMEM 0  // HOIST: probe half-logs from shared memory instead of registers
+#define UWB_Z_SMEM 1  // HOIST: z edges from shared memory (broadcast LDS) instead of registers
 #endif
 #ifndef UWB_NLI_WARPS
-#define UWB_NLI_WARPS 8
+#define UWB_NLI_WARPS 10  // hoisted FP64 kernels: x 2 CTAs = 20 warps per SM at 102 registers
+#endif                    // (8 x 2: 9.32 ms, 10 x 2: 8.73 ms on the bench workload)
+#ifndef UWB_NLI_WARPS_OTHER
+#define UWB_NLI_WARPS_OTHER 8  // per-step-load (multi-span / long-span) and mixed kernels
 #endif
 #ifndef UWB_NLI_MIN_BLOCKS
 #define UWB_NLI_MIN_BLOCKS 2
@@ -75,7 +72,11 @@ __device__ int g_nli_bounds_fail;
 #ifndef UWB_NLI_MIXED_MIN_BLOCKS
 #define UWB_NLI_MIXED_MIN_BLOCKS 3  // 80 registers: 6 warps per SMSP (10.9 -> 10.0 ms)
 #endif
-constexpr int kWarps = UWB_NLI_WARPS;  // warps per CTA
+// warps per CTA of each integrand instantiation
+template <bool HOIST, bool MIXED>
+struct WarpsFor {
+  static constexpr int value = (HOIST && !MIXED) ? UWB_NLI_WARPS : UWB_NLI_WARPS_OTHER;
+};
 constexpr unsigned kFull = 0xffffffffu;
 
 __constant__ double c_exp2_tab16[16] = UWB_EXP2_TABLE16;
@@ -140,9 +141,6 @@ struct alignas(16) PointRec {
 
 struct WarpSmem {
   PointRec pt[32];
-#if UWB_H_SMEM
-  double h[128];     // the row's probe half-log column (HOIST, K <= 8), lane order
-#endif
   double kv[32];     // |kernel|^2 of each chunk lane's evaluated point
   double nu, f, s1, s2, su, u1, lo, du2;
   int sym;           // row symmetric under u2 -> -u2 (b1 == b2: quadrants 1, 3)
@@ -250,14 +248,6 @@ struct StepTabs {
 #endif
 };
 
-__device__ __forceinline__ double& S_h(WarpSmem& S, int i) {
-#if UWB_H_SMEM
-  return S.h[i];
-#else
-  return S.kv[i & 31];  // not reached
-#endif
-}
-
 template <class T>
 __device__ __forceinline__ double TB_z(const T& tb, int i) {
 #if UWB_Z_SMEM
@@ -339,6 +329,8 @@ __device__ __forceinline__ void dev_sincos(double x, double* c_out, double* s_ou
 // table.  15 FP64 instructions where dev_sincos(phi z) took 17.
 __constant__ double c_s8[3] = {kStep8S0, kStep8S1, kStep8S2};
 __constant__ double c_c8[4] = {kStep8C0, kStep8C1, kStep8C2, kInvPio8};
+
+constexpr double kUnitInv = kInvPio8;  // 1 / (the phase unit pi/8)
 
 __device__ __forceinline__ void step_sincos8(double phi8, double z, const StepTabs& T,
                                              double* c_out, double* s_out) {
@@ -476,46 +468,17 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
     double p0 = 0.0, pp = 0.0, pc = 0.0, ps = 0.0;
     if (fast) {
       const double* ze = P.zedge + static_cast<size_t>(k) * NS + sl;
-      // table values of step b + PF are loaded while step b computes
-      // (explicit software pipeline; PF = 0: loads at their use)
-      constexpr int PF = K > 0 ? UWB_PF : 0;
-      double tv[PF + 1][6];
-#pragma unroll
-      for (int d = 0; d < PF; ++d) {
-        const int o = 16 * d;
-        tv[d][0] = __ldg(ca + o), tv[d][1] = __ldg(ca + NS + o);
-        tv[d][2] = __ldg(cb + o), tv[d][3] = __ldg(cb + NS + o);
-        tv[d][4] = __ldg(cc3 + o), tv[d][5] = __ldg(cc3 + NS + o);
-      }
 #pragma unroll(K > 0 ? K : 4)
       for (int b = 0; b < Kr; ++b) {
         const int o = 16 * b;
-        const double H = HOIST ? (UWB_H_SMEM ? S_h(const_cast<WarpSmem&>(S), o + sl) : Hr[b]) : __ldg(hl + o);
+        const double H = HOIST ? Hr[b] : __ldg(hl + o);
         double Z = HOIST ? (UWB_Z_SMEM ? TB_z(TB, o + sl) : Zr[b]) : __ldg(ze + o);
-        double lg;
-        if constexpr (PF > 0) {
-          if (b + PF < Kr) {
-            const int on = o + 16 * PF;
-            double* t = tv[(b + PF) % (PF + 1)];
-            t[0] = __ldg(ca + on), t[1] = __ldg(ca + NS + on);
-            t[2] = __ldg(cb + on), t[3] = __ldg(cb + NS + on);
-            t[4] = __ldg(cc3 + on), t[5] = __ldg(cc3 + NS + on);
-          }
-          const double* c = tv[b % (PF + 1)];
-          lg = fma(w0, c[0], -H);
-          lg = fma(w1, c[1], lg);
-          lg = fma(w2, c[2], lg);
-          lg = fma(w3, c[3], lg);
-          lg = fma(w4, c[4], lg);
-          lg = fma(w5, c[5], lg);
-        } else {
-          lg = fma(w0, __ldg(ca + o), -H);
-          lg = fma(w1, __ldg(ca + NS + o), lg);
-          lg = fma(w2, __ldg(cb + o), lg);
-          lg = fma(w3, __ldg(cb + NS + o), lg);
-          lg = fma(w4, __ldg(cc3 + o), lg);
-          lg = fma(w5, __ldg(cc3 + NS + o), lg);
-        }
+        double lg = fma(w0, __ldg(ca + o), -H);
+        lg = fma(w1, __ldg(ca + NS + o), lg);
+        lg = fma(w2, __ldg(cb + o), lg);
+        lg = fma(w3, __ldg(cb + NS + o), lg);
+        lg = fma(w4, __ldg(cc3 + o), lg);
+        lg = fma(w5, __ldg(cc3 + NS + o), lg);
         double p = step_exp2_16t(lg, TB);
         if (!FULL) {
           const bool ok = sl * Kr + b < N;
@@ -550,7 +513,7 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
 #pragma unroll(K > 0 ? K : 4)
       for (int b = 0; b < Kr; ++b) {
         const int o = 16 * b;
-        const double H = HOIST ? (UWB_H_SMEM ? S_h(const_cast<WarpSmem&>(S), o + sl) : Hr[b]) : __ldg(hl + o);
+        const double H = HOIST ? Hr[b] : __ldg(hl + o);
         double lg = fma(w0, __ldg(ca + o), -H);
         lg = fma(w1, __ldg(ca + NS + o), lg);
         lg = fma(w2, __ldg(cb + o), lg);
@@ -588,7 +551,7 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
       fim = fma(cf, ps, fim);
       // -p_0 E(z_0) / a: E = 1 when the span starts at z = 0
       if (HOIST ? z0zero : __ldg(P.zstart + k) == 0.0) {
-        if (sl == 0) fre = fma(-p0, kInvPio8, fre);
+        if (sl == 0) fre = fma(-p0, kUnitInv, fre);
       } else {
         double c0v, s0v;
         step_sincos8(phi8, __ldg(P.zstart + k), TB, &c0v, &s0v);
@@ -733,7 +696,7 @@ __device__ __forceinline__ double point_kernel_mixed(const NliParams& P, const W
     }
   }
   // 1/phi = (8/pi) / phi8 = (8/pi) rphi8
-  const double invphi = R.rphi8 * kInvPio8;
+  const double invphi = R.rphi8 * kUnitInv;
   double re = fma(fim, invphi, sre);
   double im = fma(-fre, invphi, sim);
 #pragma unroll
@@ -745,8 +708,10 @@ __device__ __forceinline__ double point_kernel_mixed(const NliParams& P, const W
 }
 
 template <int K, bool FULL, bool HOIST, bool MIXED, bool TINY>
-__global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS : UWB_NLI_MIN_BLOCKS)
+__global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
+                                  MIXED ? UWB_NLI_MIXED_MIN_BLOCKS : UWB_NLI_MIN_BLOCKS)
     nli_rows_kernel(const NliParams P) {
+  constexpr int kWarps = WarpsFor<HOIST, MIXED>::value;
   __shared__ WarpSmem s_w[kWarps];
   __shared__ StepTabs s_tabs;
   init_step_tabs(s_tabs, threadIdx.x);
@@ -773,7 +738,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
   const int per_probe = P.n_q * P.n_r;
   double Zr[K > 0 ? K : 1], Hr[K > 0 ? K : 1];
   int cur_probe = -1;
-  if (HOIST && !UWB_Z_SMEM) {
+  if (HOIST && (!UWB_Z_SMEM || MIXED)) {  // the mixed kernel keeps its z edges in registers
 #pragma unroll
     for (int b = 0; b < K; ++b) Zr[b] = __ldg(P.zedge + 16 * b + sl);
   }
@@ -798,14 +763,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
     if (HOIST && probe != cur_probe) {
       cur_probe = probe;
 #pragma unroll
-      for (int b = 0; b < K; ++b) {
-        const double hv = __ldg(P.hl2 + static_cast<size_t>(probe) * NS + 16 * b + sl);
-        if (UWB_H_SMEM && !MIXED)
-          S_h(S, 16 * b + sl) = hv;  // both half-warps store the same value
-        else
-          Hr[b] = hv;
-      }
-      if (UWB_H_SMEM) __syncwarp();
+      for (int b = 0; b < K; ++b) Hr[b] = __ldg(P.hl2 + static_cast<size_t>(probe) * NS + 16 * b + sl);
     }
     const int n_r = P.n_r;
     double du1;
@@ -935,7 +893,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIXED ? UWB_NLI_MIXED_MIN_BLOCKS 
         R.w[0] = st1.hw0 * 16.0; R.w[1] = st1.hw1 * 16.0;
         R.w[2] = st2.hw0 * 16.0; R.w[3] = st2.hw1 * 16.0;
         R.w[4] = st3.hw0 * 16.0; R.w[5] = st3.hw1 * 16.0;
-        const double phi8 = phi * kInvPio8;
+        const double phi8 = phi * kUnitInv;
         R.phi8 = phi8;
         R.rphi8 = phi != 0.0 ? __drcp_rn(phi8) : 0.0;
         R.phi = phi;
@@ -1092,6 +1050,13 @@ __global__ void finalize_channels_kernel(const FinalizeParams F) {
 
 using RowKernel = void (*)(const NliParams);
 
+// threads per CTA of an instantiation: its launch bounds (WarpsFor)
+int row_threads(RowKernel k) {
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) return 0;
+  return fa.maxThreadsPerBlock;
+}
+
 // full: every span has exactly 16 K steps (no masked lanes).
 template <int K, bool MIXED>
 RowKernel pick2(bool full, bool one_span, bool tiny) {
@@ -1227,12 +1192,13 @@ size_t row_smem(int) { return 0; }  // rows keep no per-column array (running ch
 // Shared-memory carveout: the smallest configuration that holds the CTAs one
 // SM runs (launch bounds), so the rest of the 256 KB stays L1 for the log2 rho
 // table (the default picked a 132 KB carveout for 2 x 38 KB: 124 KB of L1).
-void allow_row_smem(RowKernel k, int /*n_r*/) {
+void allow_row_smem(RowKernel k, int /*n_r*/, size_t coresident = 0) {
   // The attribute is per (device, kernel); contexts on several devices are
   // driven from concurrent host threads (optimise_launch_powers), hence the lock.
   struct Seen {
     int dev;
     RowKernel k;
+    size_t co;
   };
   static std::mutex mu;
   static Seen seen[256];
@@ -1240,8 +1206,13 @@ void allow_row_smem(RowKernel k, int /*n_r*/) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
+  Seen* slot = nullptr;
   for (int i = 0; i < n_seen; ++i)
-    if (seen[i].dev == dev && seen[i].k == k) return;
+    if (seen[i].dev == dev && seen[i].k == k) {
+      if (seen[i].co == coresident) return;
+      slot = &seen[i];
+      break;
+    }
   static const bool no_carveout = [] {  // UWB_NLI_NO_CARVEOUT=1: driver default (A/B)
     const char* e = std::getenv("UWB_NLI_NO_CARVEOUT");
     return e && e[0] == '1';
@@ -1253,12 +1224,16 @@ void allow_row_smem(RowKernel k, int /*n_r*/) {
           cudaSuccess &&
       per_sm > 0) {
     // CTAs the register file holds (the launch bounds' target)
-    const int ctas = std::max(1, 65536 / (std::max(fa.numRegs, 1) * kWarps * 32));
-    const size_t need = static_cast<size_t>(ctas) * (fa.sharedSizeBytes + 1024);
+    const int ctas = std::max(1, 65536 / (std::max(fa.numRegs, 1) * fa.maxThreadsPerBlock));
+    const size_t need = static_cast<size_t>(ctas) * (fa.sharedSizeBytes + 1024) +
+                        (coresident ? coresident + 1024 : 0);
     const int pct = static_cast<int>(std::min<size_t>(100, (100 * need + per_sm - 1) / per_sm));
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
   }
-  if (n_seen < 256) seen[n_seen++] = Seen{dev, k};
+  if (slot)
+    slot->co = coresident;
+  else if (n_seen < 256)
+    seen[n_seen++] = Seen{dev, k, coresident};
 }
 }  // namespace
 
@@ -1267,13 +1242,14 @@ int nli_ctas_per_sm(int steps, bool one_span, int n_r, bool mixed, bool tiny, bo
   if (!k) return 0;
   allow_row_smem(k, n_r);
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kWarps * 32, row_smem(n_r)) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, row_threads(k), row_smem(n_r)) !=
+      cudaSuccess)
     return 0;
   return n;
 }
 
 int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaStream_t stream,
-               cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
+               cudaEvent_t ev_k0, cudaEvent_t ev_k1, size_t coresident_smem) {
   // UWB_NLI_NO_HOIST=1 selects the per-point z/half-log loads (A/B experiments)
   static const bool no_hoist = [] {
     const char* e = std::getenv("UWB_NLI_NO_HOIST");
@@ -1288,8 +1264,8 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
   probe_halflog_kernel<<<p.n_probes, 128, 0, stream>>>(p);
   ++launches;
   if (ev_k0) cudaEventRecord(ev_k0, stream);
-  allow_row_smem(k, p.n_r);
-  k<<<grid_ctas, kWarps * 32, row_smem(p.n_r), stream>>>(p);
+  allow_row_smem(k, p.n_r, coresident_smem);
+  k<<<grid_ctas, row_threads(k), row_smem(p.n_r), stream>>>(p);
   ++launches;
   if (ev_k1) cudaEventRecord(ev_k1, stream);
   const size_t fin_smem = static_cast<size_t>(p.n_q) * p.n_r * sizeof(double);

@@ -119,8 +119,11 @@ inline void append_span_tables(const double* edge, const double* mid, const doub
 // integrand rows (persistent, grid_ctas CTAs), per-probe and per-channel
 // finalize.  ev_k0/ev_k1 (may be null) bracket the integrand kernel.
 // Returns the number of kernel launches (memset excluded).
+// coresident_smem: shared memory another kernel must find free on an SM next
+// to the integrand's CTAs (the overlapped batch's Raman ODE); it raises the
+// integrand's shared-memory carveout accordingly (0: smallest carveout, most L1).
 int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaStream_t stream,
-               cudaEvent_t ev_k0, cudaEvent_t ev_k1);
+               cudaEvent_t ev_k0, cudaEvent_t ev_k1, size_t coresident_smem = 0);
 
 // CTAs per SM the integrand kernel reaches for a given step count.
 int nli_ctas_per_sm(int steps, bool one_span, int n_r, bool mixed = false, bool tiny = false,

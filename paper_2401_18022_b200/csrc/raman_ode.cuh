@@ -67,6 +67,10 @@ size_t ode_gwork_double2(int n);
 int launch_raman_ode(OdeParams P, const double* freq, const double* psd, double bch,
                      const double* aeff, double aeff_ref, cudaStream_t st);
 
+// Shared memory (dynamic + static) of the ODE CTA launch_raman_ode issues for
+// n channels with the given gain table (0 when it runs from global memory).
+size_t raman_ode_smem_bytes(const OdeParams& P);
+
 // The (warps, channels per thread) split launch_raman_ode picks for n
 // channels (UWB_ODE_SPLIT="W,EPT" overrides it for experiments).
 void ode_split(int n, int* warps, int* ept);

@@ -485,7 +485,12 @@ int uwb_evaluate_link_resident(uwb_ctx* c, const double* psd_dev, double* report
 static int ensure_batch_state(uwb_ctx* c) {
   if (c->batch) return UWB_OK;
   auto* B = new uwb_ctx::BatchState();
-  cudaError_t e = cudaStreamCreateWithFlags(&B->s_ode, cudaStreamNonBlocking);
+  // the ODE stream gets the highest priority: when the ODE of evaluation e + 1 and
+  // the integrand of evaluation e become ready together, the block scheduler
+  // places the one ODE CTA first and the integrand's CTAs fill around it
+  int lo_prio = 0, hi_prio = 0;
+  cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+  cudaError_t e = cudaStreamCreateWithPriority(&B->s_ode, cudaStreamNonBlocking, hi_prio);
   for (cudaEvent_t* ev : {&B->ev_start, &B->ev_ode[0], &B->ev_ode[1], &B->ev_nli[0], &B->ev_nli[1]})
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
   c->batch = B;
@@ -525,7 +530,11 @@ int uwb_evaluate_link_many(uwb_ctx* c, int n_eval, const double* psd_host, doubl
     if (rc) return rc;
     uwb_ctx::BatchState& B = *c->batch;
     const int per_sm = pr->grid_ctas / c->sm_count;
-    const int grid = std::max(1, pr->grid_ctas - per_sm);
+    static const int free_ctas = [] {  // UWB_BATCH_FREE: integrand CTAs left out (A/B)
+      const char* e = std::getenv("UWB_BATCH_FREE");
+      return e ? std::atoi(e) : -1;
+    }();
+    const int grid = std::max(1, pr->grid_ctas - (free_ctas >= 0 ? free_ctas : per_sm));
     NliParams Pb[2] = {pr->P, pr->P};
     Pb[0].probe_work = Pb[1].probe_work = nullptr;  // two evaluations in flight
     FinalizeParams Fb[2] = {pr->F, pr->F};
@@ -543,6 +552,9 @@ int uwb_evaluate_link_many(uwb_ctx* c, int n_eval, const double* psd_host, doubl
     Ob[1].coef_u = wb + tab + 2 * n;
     Ob[1].coef_v = wb + tab + 3 * n;
     Ob[1].gwork = pr->O.gwork + ode_gwork_double2(static_cast<int>(n));
+    // the ODE CTA must find its shared memory free on an SM that runs
+    // integrand CTAs: the integrand's carveout leaves room for it
+    const size_t ode_smem = raman_ode_smem_bytes(Ob[0]);
     cudaEventRecord(B.ev_start, st);
     cudaStreamWaitEvent(B.s_ode, B.ev_start, 0);  // uploads / status reset first
     for (int e = 0; e < n_eval; ++e) {
@@ -555,7 +567,7 @@ int uwb_evaluate_link_many(uwb_ctx* c, int n_eval, const double* psd_host, doubl
       if (lo < 0) return fail(UWB_CUDA_ERROR, "raman ODE launch failed");
       cudaEventRecord(B.ev_ode[b], B.s_ode);
       cudaStreamWaitEvent(st, B.ev_ode[b], 0);
-      const int ln = launch_nli(Pb[b], Fb[b], grid, st, nullptr, nullptr);
+      const int ln = launch_nli(Pb[b], Fb[b], grid, st, nullptr, nullptr, ode_smem);
       if (ln < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
       if ((rc = run_report(c, st, &Lb[b]))) return rc;
       xfer(c, d_rep + e * rl, pr->L.out, rl * sizeof(double), cudaMemcpyDeviceToDevice, st);

@@ -8,9 +8,11 @@ GPUs:
 
 * each rank runs the (tiny, replicated) Raman ODE and the NLI of its own
   channels -- no collective inside the data path;
-* the per-channel eta vectors (zeros outside each rank's channels) are
-  combined by ONE all-reduce(sum) -- x + 0 == x exactly, so the result is
-  bit-identical to a single-GPU run whatever the partition;
+* the per-channel eta values are exchanged by ONE all-gather: every rank
+  packs its own channels' eta (in its partition order, padded to the largest
+  share) and scatters the gathered slices into the full vector by the
+  partition every rank knows -- pure copies, so the result is bit-identical to
+  a single-GPU run whatever the partition;
 * the SNR report is then assembled on every rank from the full vector.
 
 Partitioning: channels are dealt by longest-processing-time (LPT) on a cost
@@ -58,6 +60,42 @@ def active_channels(grid) -> np.ndarray:
     return np.flatnonzero((np.asarray(grid.guard) == 0) & (np.asarray(grid.psd) > 0.0))
 
 
+class EtaGather:
+    """The per-COI eta exchange as one all-gather (north star item 4).
+
+    Rank r owns the channels parts[r]; pack() copies its values into a slot
+    of width m = max |parts| and gather() all-gathers the [world, m] slots and
+    scatters them back into the full eta vector by the (shared) partition.
+    Works for CUDA tensors (NCCL) and CPU tensors (gloo)."""
+
+    def __init__(self, parts, rank: int, device):
+        import torch
+
+        self.world, self.rank = len(parts), rank
+        self.m = max(1, max(len(p) for p in parts))
+        idx = np.zeros((self.world, self.m), dtype=np.int64)
+        valid = np.zeros((self.world, self.m), dtype=bool)
+        for r, p in enumerate(parts):
+            idx[r, :len(p)] = p
+            valid[r, :len(p)] = True
+        self.mine = torch.as_tensor(np.asarray(parts[rank], dtype=np.int64), device=device)
+        self.dst = torch.as_tensor(idx[valid], device=device)
+        self.valid = torch.as_tensor(valid.reshape(-1), device=device)
+
+    def gather(self, eta, group=None):
+        import torch
+        import torch.distributed as dist
+
+        if not (dist.is_available() and dist.is_initialized()) or self.world == 1:
+            return eta
+        send = torch.zeros(self.m, dtype=eta.dtype, device=eta.device)
+        send[:len(self.mine)] = eta[self.mine]
+        recv = torch.empty(self.world * self.m, dtype=eta.dtype, device=eta.device)
+        dist.all_gather_into_tensor(recv, send, group=group)
+        eta[self.dst] = recv[self.valid]
+        return eta
+
+
 def allreduce_eta(eta, group=None):
     """Sum the per-rank eta vectors in place (zeros outside each rank's
     channels).  Works for CUDA tensors (NCCL) and CPU tensors (gloo)."""
@@ -72,7 +110,7 @@ class ShardedLink:
     """Full SNR evaluation on N GPUs: this rank's share of the channels.
 
     Wraps gn_integral.ResidentLink: run(psd_dev) = noise (ODE + this rank's
-    NLI) -> NCCL all-reduce of eta -> SNR report (device-resident throughout).
+    NLI) -> NCCL all-gather of eta -> SNR report (device-resident throughout).
     """
 
     def __init__(self, fibre, grid, cfg, rank: int, world: int, engine=None, cost=None):
@@ -103,6 +141,7 @@ class ShardedLink:
 
         self.eta = torch.as_tensor(_Cai(), device=dev)
         self.report_len = self.res.report_len
+        self.exchange = EtaGather(self.parts, rank, dev)
 
     def rebalance(self):
         """Re-deal the channels by LPT on the per-channel work the last
@@ -135,7 +174,7 @@ class ShardedLink:
             return self.eng.last_launches()
         self.res.run_noise(psd_ptr, stream_ptr)
         n = self.eng.last_launches()
-        allreduce_eta(self.eta)
+        self.exchange.gather(self.eta)
         self.res.run_report(report_ptr, stream_ptr)
         return n + self.eng.last_launches()
 

@@ -14,7 +14,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2401_18022_b200.multigpu import active_channels, allreduce_eta, partition_channels
+from paper_2401_18022_b200.multigpu import (EtaGather, active_channels, allreduce_eta,
+                                            partition_channels)
 
 
 def test_partition_covers_and_balances():
@@ -58,14 +59,23 @@ def _worker(rank, world, port, q):
         guard = ga["guard"]
         psd = ga["psd"]
 
-    mine = partition_channels(active_channels(G), world)[rank]
+    parts = partition_channels(active_channels(G), world)
+    mine = parts[rank]
     full = O.all_channels_nli(case, prep)
     eta = torch.zeros(len(ga["freq"]), dtype=torch.float64)
     # rank-local evaluation: only this rank's channels are non-zero
     eta[mine] = torch.from_numpy(full["eta"][mine])
+    eta2 = eta.clone()
     allreduce_eta(eta)
+    # the bench's exchange: one all-gather of the packed per-rank slices (an
+    # uneven LPT deal, so the padding path is exercised too)
+    cost = np.arange(len(ga["freq"]), dtype=np.float64)[active_channels(G)] ** 2
+    parts2 = partition_channels(active_channels(G), world, cost)
+    eta3 = torch.zeros_like(eta2)
+    eta3[parts2[rank]] = torch.from_numpy(full["eta"][parts2[rank]])
+    EtaGather(parts2, rank, torch.device("cpu")).gather(eta3)
     if rank == 0:
-        q.put((eta.numpy().copy(), full["eta"]))
+        q.put((eta.numpy().copy(), full["eta"], eta3.numpy().copy()))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -77,11 +87,12 @@ def test_two_rank_allreduce_is_bit_identical():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    got, want = q.get(timeout=180)
+    got, want, gathered = q.get(timeout=180)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     assert np.array_equal(got, want)
+    assert np.array_equal(gathered, want)
 
 
 def _gpu_worker(rank, world, port, q):
