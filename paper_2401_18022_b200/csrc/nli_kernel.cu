@@ -1264,7 +1264,11 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
   probe_halflog_kernel<<<p.n_probes, 128, 0, stream>>>(p);
   ++launches;
   if (ev_k0) cudaEventRecord(ev_k0, stream);
-  allow_row_smem(k, p.n_r, coresident_smem);
+  static const bool no_co = [] {  // UWB_NLI_NO_CO=1: ignore coresident_smem (A/B)
+    const char* e = std::getenv("UWB_NLI_NO_CO");
+    return e && e[0] == '1';
+  }();
+  allow_row_smem(k, p.n_r, no_co ? 0 : coresident_smem);
   k<<<grid_ctas, row_threads(k), row_smem(p.n_r), stream>>>(p);
   ++launches;
   if (ev_k1) cudaEventRecord(ev_k1, stream);

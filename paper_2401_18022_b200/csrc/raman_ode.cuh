@@ -64,8 +64,11 @@ size_t ode_gwork_double2(int n);
 // Fills the per-channel coupling factors from the launch PSD and runs the
 // one-CTA ODE kernel.  Returns kernel launches issued, or < 0 on failure
 // (-1: n out of range, -2: launch error).
+// coresident: the ODE runs beside the integrand (overlapped batch): the
+// 224-register instantiation, which fits in a partly occupied SM.
 int launch_raman_ode(OdeParams P, const double* freq, const double* psd, double bch,
-                     const double* aeff, double aeff_ref, cudaStream_t st);
+                     const double* aeff, double aeff_ref, cudaStream_t st,
+                     bool coresident = false);
 
 // Shared memory (dynamic + static) of the ODE CTA launch_raman_ode issues for
 // n channels with the given gain table (0 when it runs from global memory).

@@ -524,8 +524,10 @@ int uwb_evaluate_link_many(uwb_ctx* c, int n_eval, const double* psd_host, doubl
     // Overlapped batch: the Raman ODE of evaluation e + 1 (one small CTA, on
     // its own stream) runs while the integrand of evaluation e occupies the
     // other SMs.  Two ODE output buffers alternate; the integrand grid leaves
-    // one SM's worth of CTAs free and the ODE uses 128 threads x <= 255
-    // registers, so it fits beside an integrand CTA.
+    // one SM's worth of CTAs free, and the ODE runs its 224-register build
+    // (7,168 registers per warp: it fits in an SM sub-partition beside three
+    // 96-register integrand warps), so it finds room wherever the integrand's
+    // CTAs were placed; the integrand's carveout leaves it shared memory.
     int rc = ensure_batch_state(c);
     if (rc) return rc;
     uwb_ctx::BatchState& B = *c->batch;
@@ -563,7 +565,7 @@ int uwb_evaluate_link_many(uwb_ctx* c, int n_eval, const double* psd_host, doubl
       Pb[b].psd = Fb[b].psd = Lb[b].psd = psd_e;
       if (e >= 2) cudaStreamWaitEvent(B.s_ode, B.ev_nli[b], 0);  // eval e-2 done with buffer b
       const int lo = launch_raman_ode(Ob[b], pr->P.freq, psd_e, pr->P.bch, pr->d_aeff, pr->aeff_ref,
-                                      B.s_ode);
+                                      B.s_ode, /*coresident=*/true);
       if (lo < 0) return fail(UWB_CUDA_ERROR, "raman ODE launch failed");
       cudaEventRecord(B.ev_ode[b], B.s_ode);
       cudaStreamWaitEvent(st, B.ev_ode[b], 0);

@@ -19,6 +19,9 @@ p = argparse.ArgumentParser()
 p.add_argument("--n-eval", type=int, default=56)
 p.add_argument("--n-r", type=int, default=150)
 p.add_argument("--density", type=float, default=1.4)
+p.add_argument("--interleave", type=int, default=0,
+               help="batches of n_eval, each preceded by one single evaluation (the optimiser's "
+                    "value + gradient pattern); 0 = one batch")
 a = p.parse_args()
 eng = uwb.Engine(0)
 grid = uwb.make_default_uwb_grid()
@@ -30,9 +33,16 @@ rng = np.random.default_rng(20240131)
 base = np.asarray(grid.psd)
 psd = np.stack([base * 10 ** (rng.uniform(-0.5, 0.5, base.size) / 10) for _ in range(a.n_eval)])
 res.run_many(psd[:2])
-t0 = time.perf_counter()
-loss, reps = res.run_many(psd, reports=True)
-dt = time.perf_counter() - t0
-print(json.dumps({"n_eval": a.n_eval, "n_r": a.n_r, "density": a.density, "wall_s": dt,
+if a.interleave:
+    t0 = time.perf_counter()
+    for _ in range(a.interleave):
+        res.run_many(psd[:1])
+        loss, reps = res.run_many(psd, reports=True)
+    dt = (time.perf_counter() - t0) / a.interleave
+else:
+    t0 = time.perf_counter()
+    loss, reps = res.run_many(psd, reports=True)
+    dt = time.perf_counter() - t0
+print(json.dumps({"n_eval": a.n_eval, "interleave": a.interleave, "n_r": a.n_r, "density": a.density, "wall_s": dt,
                   "ms_per_eval": dt / a.n_eval * 1e3, "serial": os.environ.get("UWB_BATCH_SERIAL", "0"),
                   "loss_sum": float(np.sum(loss)), "eta_sum": float(np.sum(reps[:, :grid.size()]))}))
