@@ -61,8 +61,8 @@ __device__ int g_nli_bounds_fail;
 #define UWB_Z_SMEM 1  // HOIST: z edges from shared memory (broadcast LDS) instead of registers
 #endif
 #ifndef UWB_NLI_WARPS
-#define UWB_NLI_WARPS 10  // hoisted FP64 kernels: x 2 CTAs = 20 warps per SM at 102 registers
-#endif                    // (8 x 2: 9.32 ms, 10 x 2: 8.73 ms on the bench workload)
+#define UWB_NLI_WARPS 8  // hoisted FP64 kernels (8-lane segments): x 2 CTAs, 128 registers
+#endif                   // (8.48 ms on the bench workload; 10 x 2 at 96 registers: 8.52)
 #ifndef UWB_NLI_WARPS_OTHER
 #define UWB_NLI_WARPS_OTHER 8  // per-step-load (multi-span / long-span) and mixed kernels
 #endif
@@ -139,9 +139,18 @@ struct alignas(16) PointRec {
   double pad;
 };
 
+#ifndef UWB_SEG8
+#define UWB_SEG8 1  // hoisted FP64 kernels: 8-lane segments over 2K steps (point_kernel8)
+#endif
+#if UWB_SEG8 && !UWB_Z_SMEM
+#error "UWB_SEG8 reads the z edges from shared memory (UWB_Z_SMEM)"
+#endif
 struct WarpSmem {
   PointRec pt[32];
   double kv[32];     // |kernel|^2 of each chunk lane's evaluated point
+#if UWB_SEG8
+  alignas(16) double h[128];  // the row's probe half-log column (point_kernel8), lane order
+#endif
   double nu, f, s1, s2, su, u1, lo, du2;
   int sym;           // row symmetric under u2 -> -u2 (b1 == b2: quadrants 1, 3)
 };
@@ -247,6 +256,14 @@ struct StepTabs {
   double z[128];  // the span's end-edge positions (HOIST, K <= 8), lane order
 #endif
 };
+
+__device__ __forceinline__ double* S_h(WarpSmem& S) {
+#if UWB_SEG8
+  return S.h;
+#else
+  return nullptr;  // not reached
+#endif
+}
 
 template <class T>
 __device__ __forceinline__ double TB_z(const T& tb, int i) {
@@ -575,6 +592,160 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
   return re * re + im * im;
 }
 
+// point_kernel for one 8-lane segment (single span, FP64; UWB_SEG8): a warp
+// evaluates four points at a time.  Lane s8 takes the steps of the two
+// 16-lane-layout lanes 2 s8 and 2 s8 + 1, i.e. the 2K CONTIGUOUS steps
+// [2 s8 K, 2 s8 K + 2K): run A = first K, run B = next K.  In the lane-ordered
+// table those two lanes' values for a given b sit side by side, so ONE 16-byte
+// load serves both runs (three LDG.128 per step pair instead of six LDG.64 per
+// step: the same L1 wavefronts, half the load instructions).  Run A's last step
+// pairs with run B's first inside the lane; run B's last pairs with the next
+// lane's first (one shuffle); the per-point record loads, the boundary shuffle
+// and the 3-level reduction tree are amortised over 2K steps instead of K.
+// The probe half-logs come from a per-warp shared column (S.h), the z edges
+// from the CTA-wide one, both as 16-byte pairs.
+template <int K, bool FULL, bool TINY>
+__device__ __forceinline__ double point_kernel8(const NliParams& P, const WarpSmem& S, int idx,
+                                                int s8, bool fast, bool z0zero,
+                                                const StepTabs& TB) {
+  constexpr int NS = 16 * K;
+  const PointRec& R = S.pt[idx];
+  const double2 wa = *reinterpret_cast<const double2*>(&R.w[0]);
+  const double2 wb = *reinterpret_cast<const double2*>(&R.w[2]);
+  const double2 wc = *reinterpret_cast<const double2*>(&R.w[4]);
+  const double2 ph = *reinterpret_cast<const double2*>(&R.phi8);
+  const int4 cl = *reinterpret_cast<const int4*>(&R.col[0]);
+  const double phi8 = ph.x;
+  const double w0 = wa.x, w1 = wa.y, w2 = wb.x, w3 = wb.y, w4 = wc.x, w5 = wc.y;
+  const int l2 = 2 * s8;
+  UWB_BOUND(cl.x >= 0 && cl.y >= 0 && cl.z >= 0 && max(cl.x, max(cl.y, cl.z)) + 2 * NS <=
+                                                       (P.n_ch + 1) * NS);
+  const double2* ca = reinterpret_cast<const double2*>(P.log2rho + cl.x + l2);
+  const double2* cb = reinterpret_cast<const double2*>(P.log2rho + cl.y + l2);
+  const double2* cc3 = reinterpret_cast<const double2*>(P.log2rho + cl.z + l2);
+  const double2* hs = reinterpret_cast<const double2*>(S_h(const_cast<WarpSmem&>(S)) + l2);
+  const double2* zs = reinterpret_cast<const double2*>(TB.z + l2);
+  constexpr int NS2 = NS / 2;  // the column stride in double2 units
+  const int N = P.steps;
+  const int mA = l2 * K, mB = mA + K;  // first step of run A / run B
+  double fre = 0.0, fim = 0.0, sre = 0.0, sim = 0.0;
+  double pA0 = 0.0, pB0 = 0.0, ppA = 0.0, ppB = 0.0, pcA = 0.0, psA = 0.0, pcB = 0.0, psB = 0.0;
+  if (fast) {
+#pragma unroll
+    for (int b = 0; b < K; ++b) {
+      const int o = 8 * b;  // 16 b doubles = 8 b double2
+      const double2 H = hs[o];
+      double2 Z = zs[o];
+      const double2 a0 = __ldg(ca + o), a1 = __ldg(ca + NS2 + o);
+      const double2 b0 = __ldg(cb + o), b1 = __ldg(cb + NS2 + o);
+      const double2 c0 = __ldg(cc3 + o), c1 = __ldg(cc3 + NS2 + o);
+      double lgA = fma(w0, a0.x, -H.x), lgB = fma(w0, a0.y, -H.y);
+      lgA = fma(w1, a1.x, lgA), lgB = fma(w1, a1.y, lgB);
+      lgA = fma(w2, b0.x, lgA), lgB = fma(w2, b0.y, lgB);
+      lgA = fma(w3, b1.x, lgA), lgB = fma(w3, b1.y, lgB);
+      lgA = fma(w4, c0.x, lgA), lgB = fma(w4, c0.y, lgB);
+      lgA = fma(w5, c1.x, lgA), lgB = fma(w5, c1.y, lgB);
+      double pA = step_exp2_16t(lgA, TB), pB = step_exp2_16t(lgB, TB);
+      if (!FULL) {
+        const bool okA = mA + b < N, okB = mB + b < N;
+        pA = okA ? pA : 0.0;
+        Z.x = okA ? Z.x : 0.0;
+        pB = okB ? pB : 0.0;
+        Z.y = okB ? Z.y : 0.0;
+      }
+      double cA, sA, cB, sB;
+      step_sincos8(phi8, Z.x, TB, &cA, &sA);
+      step_sincos8(phi8, Z.y, TB, &cB, &sB);
+      if (b == 0) {
+        pA0 = pA;
+        pB0 = pB;
+      } else {  // (p_{m-1} - p_m) E_m, E_m = end edge of the previous step
+        const double cfA = ppA - pA, cfB = ppB - pB;
+        fre = fma(cfA, pcA, fre);
+        fim = fma(cfA, psA, fim);
+        fre = fma(cfB, pcB, fre);
+        fim = fma(cfB, psB, fim);
+      }
+      ppA = pA, pcA = cA, psA = sA;
+      ppB = pB, pcB = cB, psB = sB;
+    }
+    // run A's last step pairs with run B's first
+    const double cf = ppA - pB0;
+    fre = fma(cf, pcA, fre);
+    fim = fma(cf, psA, fim);
+  } else {
+    const double phi = R.phi;
+    const double2* zm = reinterpret_cast<const double2*>(P.zmid + l2);
+    const double2* wd = reinterpret_cast<const double2*>(P.width + l2);
+#pragma unroll
+    for (int b = 0; b < K; ++b) {
+      const int o = 8 * b;
+      const double2 H = hs[o];
+      const double2 a0 = __ldg(ca + o), a1 = __ldg(ca + NS2 + o);
+      const double2 b0 = __ldg(cb + o), b1 = __ldg(cb + NS2 + o);
+      const double2 c0 = __ldg(cc3 + o), c1 = __ldg(cc3 + NS2 + o);
+      double lgA = fma(w0, a0.x, -H.x), lgB = fma(w0, a0.y, -H.y);
+      lgA = fma(w1, a1.x, lgA), lgB = fma(w1, a1.y, lgB);
+      lgA = fma(w2, b0.x, lgA), lgB = fma(w2, b0.y, lgB);
+      lgA = fma(w3, b1.x, lgA), lgB = fma(w3, b1.y, lgB);
+      lgA = fma(w4, c0.x, lgA), lgB = fma(w4, c0.y, lgB);
+      lgA = fma(w5, c1.x, lgA), lgB = fma(w5, c1.y, lgB);
+      const double pv[2] = {step_exp2_16t(lgA, TB), step_exp2_16t(lgB, TB)};
+      const double2 wm2 = __ldg(wd + o), zm2 = __ldg(zm + o);
+      const double wmv[2] = {wm2.x, wm2.y}, zmv[2] = {zm2.x, zm2.y};
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        // sinc(x), |x| = |phi| w / 2 <= 5e-5 here: 1 - x^2/6 + x^4/120 is exact
+        const double x = 0.5 * phi * wmv[r];
+        const double x2 = x * x;
+        const double sinc = fma(x2, fma(x2, 1.0 / 120.0, -1.0 / 6.0), 1.0);
+        double w = pv[r] * wmv[r] * sinc;
+        if (!FULL) w = ((r ? mB : mA) + b < N) ? w : 0.0;
+        const double a = phi * zmv[r];
+        double cs, sn;
+        if constexpr (TINY) {
+          const double a2 = a * a;
+          cs = fma(a2, fma(a2, fma(a2, -1.0 / 720.0, 1.0 / 24.0), -0.5), 1.0);
+          sn = fma(a * a2, fma(a2, fma(a2, -1.0 / 5040.0, 1.0 / 120.0), -1.0 / 6.0), a);
+        } else {
+          dev_sincos(a, &cs, &sn);
+        }
+        sre = fma(w, cs, sre);
+        sim = fma(w, sn, sim);
+      }
+    }
+  }
+  // run B's last step pairs with the next lane's first (p_N = 0); all four
+  // segments reach this shuffle whatever their branch
+  double pn = __shfl_down_sync(kFull, pA0, 1, 8);
+  if (fast) {
+    if (s8 == 7) pn = 0.0;
+    const double cf = ppB - pn;
+    fre = fma(cf, pcB, fre);
+    fim = fma(cf, psB, fim);
+    // -p_0 E(z_0) / a: E = 1 when the span starts at z = 0
+    if (z0zero) {
+      if (s8 == 0) fre = fma(-pA0, kUnitInv, fre);
+    } else {
+      double c0v, s0v;
+      step_sincos8(phi8, __ldg(P.zstart), TB, &c0v, &s0v);
+      if (s8 == 0) {
+        fre = fma(-pA0, c0v, fre);
+        fim = fma(-pA0, s0v, fim);
+      }
+    }
+  }
+  const double rphi8 = ph.y;
+  double re = fma(fim, rphi8, sre);
+  double im = fma(-fre, rphi8, sim);
+#pragma unroll
+  for (int o = 4; o >= 1; o >>= 1) {
+    re += __shfl_xor_sync(kFull, re, o, 8);
+    im += __shfl_xor_sync(kFull, im, o, 8);
+  }
+  return re * re + im * im;
+}
+
 // point_kernel in compensated FP32 (see mixed_exp2_16 above): same lane
 // layout, same summation by parts, same fast/slow split; lane partial sums in
 // FP32, everything across lanes in FP64.
@@ -762,8 +933,14 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
     }
     if (HOIST && probe != cur_probe) {
       cur_probe = probe;
+      if constexpr (UWB_SEG8 && !MIXED) {
+        __syncwarp();  // the previous probe's column is no longer read
+        for (int m = lane; m < NS; m += 32) S_h(S)[m] = __ldg(P.hl2 + static_cast<size_t>(probe) * NS + m);
+        __syncwarp();
+      } else {
 #pragma unroll
-      for (int b = 0; b < K; ++b) Hr[b] = __ldg(P.hl2 + static_cast<size_t>(probe) * NS + 16 * b + sl);
+        for (int b = 0; b < K; ++b) Hr[b] = __ldg(P.hl2 + static_cast<size_t>(probe) * NS + 16 * b + sl);
+      }
     }
     const int n_r = P.n_r;
     double du1;
@@ -905,16 +1082,28 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
       n_act_row += __popc(am);
       // warp-uniform trip count: with an odd count the idle half-warp repeats
       // its partner's point (same branch, result dropped) instead of diverging
-      for (int base = 0; base < n_need; base += 2) {
-        const bool ok = base + seg < n_need;
-        const int idx = ok ? base + seg : base;
-        double kv;
-        if constexpr (MIXED)
-          kv = point_kernel_mixed<K, FULL, HOIST>(P, S, idx, probe, sl, Zr, Hr);
-        else
-          kv = point_kernel<K, FULL, HOIST, TINY>(P, S, idx, probe, sl, idx < n_fast, z0zero,
-                                                  s_tabs, Zr, Hr);
-        if (ok && sl == 0) S.kv[S.pt[idx].src] = kv;
+      if constexpr (UWB_SEG8 && HOIST && !MIXED) {
+        // four points per warp, one per 8-lane segment (idle segments repeat
+        // point `base`, result dropped)
+        const int sg = lane >> 3, s8 = lane & 7;
+        for (int base = 0; base < n_need; base += 4) {
+          const bool ok = base + sg < n_need;
+          const int idx = ok ? base + sg : base;
+          const double kv = point_kernel8<K, FULL, TINY>(P, S, idx, s8, idx < n_fast, z0zero, s_tabs);
+          if (ok && s8 == 0) S.kv[S.pt[idx].src] = kv;
+        }
+      } else {
+        for (int base = 0; base < n_need; base += 2) {
+          const bool ok = base + seg < n_need;
+          const int idx = ok ? base + seg : base;
+          double kv;
+          if constexpr (MIXED)
+            kv = point_kernel_mixed<K, FULL, HOIST>(P, S, idx, probe, sl, Zr, Hr);
+          else
+            kv = point_kernel<K, FULL, HOIST, TINY>(P, S, idx, probe, sl, idx < n_fast, z0zero,
+                                                    s_tabs, Zr, Hr);
+          if (ok && sl == 0) S.kv[S.pt[idx].src] = kv;
+        }
       }
       __syncwarp();
       UWB_BOUND(!valid || (j >= 0 && j < n_r));
