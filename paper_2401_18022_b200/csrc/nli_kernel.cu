@@ -163,26 +163,21 @@ __constant__ double c_e4[6] = {kE4c1, kE4c2, kE4c3, kE4c4, kE4c5, kE4c6};
 #define UWB_FAST_POLY 2
 #endif
 // Step kernels for 2^(r/16), sin and cos on the reduced ranges, shorter than
-// the ulp-accurate ones (Chebyshev fits).  UWB_FAST_POLY=2 (default): 2^x
-// degree 4 (max relative error 5e-12), sin degree 7 (3.7e-14 absolute), cos
-// degree 6 (1.7e-12 absolute); =1: 2^x degree 5 (9e-15), cos degree 8
-// (2.2e-16); =0: the ulp-accurate kernels.  They only enter the per-step
-// phasor sums, not a discrete decision, so the row setup keeps the
-// full-accuracy dev_exp2_16 (its coordinates decide the active set).  Five
-// DFMA fewer per step at level 2 (10.26 -> 9.40 ms); eta vs the reference
-// moves from 3.06e-12 to 3.17e-12 on the 589-ch golden and to <= 6.2e-13 on
-// the 11-channel goldens (tests: 1e-9; north star: 1e-6).
-__constant__ double c_e5f[5] = {0.04332169878499661, 0.0009383847926296655, 1.3550807777515591e-05,
-                                1.4676387236639375e-07, 1.2716084569825118e-09};
+// the ulp-accurate ones (Chebyshev fits): 2^x degree 4 (max relative error
+// 5e-12), sin degree 7 (3.7e-14 absolute), cos degree 6 (1.7e-12 absolute).
+// They only enter the per-step phasor sums, not a discrete decision, so the
+// row setup keeps the full-accuracy dev_exp2_16 (its coordinates decide the
+// active set).  UWB_FAST_POLY selects the sinc branch's dev_sincos kernels
+// (2: these fits, 1: cos degree 8, 0: ulp-accurate); the fast branch always
+// runs step_exp2_16t / step_sincos8.  eta vs the reference: 3.2e-12 on the
+// 589-ch golden, <= 6.2e-13 on the 11-channel goldens (tests: 1e-9).
+// The coefficients live in uwb_devmath.cuh (kStep*), where
+// tests/test_devmath.py checks them on the host.
 __constant__ double c_s3f[3] = {kStepS0, kStepS1, kStepS2};
 __constant__ double c_c4f[4] = {-0.4999999999999954, 0.0416666666627131, -0.0013888883764931453,
                                 2.478033379585741e-05};
-#if UWB_FAST_POLY >= 2
-// the step kernels' coefficients live in uwb_devmath.cuh (kStep*), where
-// tests/test_devmath.py checks them on the host
 __constant__ double c_e4f[4] = {kStepE0, kStepE1, kStepE2, kStepE3};
 __constant__ double c_c3f[3] = {kStepC0, kStepC1, kStepC2};
-#endif
 
 // 2^(j/16) for dev_exp2_16, filled by each CTA at start.  A file-scope
 // __shared__ array (not a generic pointer) so the lookup is one LDS.
@@ -202,29 +197,6 @@ __device__ __forceinline__ double dev_exp2_16(double x) {
   p = fma(p, r, 1.0);
   const double s = s_exp2_tab[k & 15] * p;
   return __hiloint2double(__double2hiint(s) + ((k >> 4) << 20), __double2loint(s));
-}
-
-__device__ __forceinline__ double step_exp2_16(double x) {
-  if (!UWB_FAST_POLY) return dev_exp2_16(x);
-  const double t = x + kMagic;
-  const int k = __double2loint(t);
-  const double r = x - (t - kMagic);
-#if UWB_FAST_POLY >= 2
-  double p = fma(r, c_e4f[3], c_e4f[2]);
-  p = fma(p, r, c_e4f[1]);
-  p = fma(p, r, c_e4f[0]);
-  p = fma(p, r, 1.0);
-  const double s = s_exp2_tab[k & 15] * p;
-  return __hiloint2double(__double2hiint(s) + ((k >> 4) << 20), __double2loint(s));
-#else
-  double p = fma(r, c_e5f[4], c_e5f[3]);
-  p = fma(p, r, c_e5f[2]);
-  p = fma(p, r, c_e5f[1]);
-  p = fma(p, r, c_e5f[0]);
-  p = fma(p, r, 1.0);
-  const double s = s_exp2_tab[k & 15] * p;
-  return __hiloint2double(__double2hiint(s) + ((k >> 4) << 20), __double2loint(s));
-#endif
 }
 
 // (cos x, sin x) for |x| < 2^50 by a 16-entry full-circle table: x = k pi/8
