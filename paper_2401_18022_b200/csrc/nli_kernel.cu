@@ -134,9 +134,10 @@ struct alignas(16) PointRec {
   double phi8, rphi8;  // phi 8/pi (the fast branch's phase in units of pi/8) and 1/phi8
                        // (0 when phi == 0: no fast span then)
   int col[3];          // element offset (i0 * NS) of each stencil's first column
-  int src;             // chunk-local column of the listed point
+  int src;             // chunk-local column of the listed point (point_kernel8 path: 1 = fast)
   double phi;          // phase mismatch itself (sinc branch, fast/slow test of later spans)
-  double pad;
+  double pws;          // point_kernel8 path: p1 p2 p3 of the column plus that of the mirror
+                       // column sharing its |K|^2 (0 when none)
 };
 
 #ifndef UWB_SEG8
@@ -146,7 +147,7 @@ struct alignas(16) PointRec {
 #error "UWB_SEG8 reads the z edges from shared memory (UWB_Z_SMEM)"
 #endif
 struct WarpSmem {
-  PointRec pt[32];
+  PointRec pt[36];   // a chunk's listed points, plus up to 3 carried over (point_kernel8 path)
   double kv[32];     // |kernel|^2 of each chunk lane's evaluated point
 #if UWB_SEG8
   alignas(16) double h[128];  // the row's probe half-log column (point_kernel8), lane order
@@ -578,8 +579,7 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
 // from the CTA-wide one, both as 16-byte pairs.
 template <int K, bool FULL, bool TINY>
 __device__ __forceinline__ double point_kernel8(const NliParams& P, const WarpSmem& S, int idx,
-                                                int s8, bool fast, bool z0zero,
-                                                const StepTabs& TB) {
+                                                int s8, bool z0zero, const StepTabs& TB) {
   constexpr int NS = 16 * K;
   const PointRec& R = S.pt[idx];
   const double2 wa = *reinterpret_cast<const double2*>(&R.w[0]);
@@ -587,6 +587,7 @@ __device__ __forceinline__ double point_kernel8(const NliParams& P, const WarpSm
   const double2 wc = *reinterpret_cast<const double2*>(&R.w[4]);
   const double2 ph = *reinterpret_cast<const double2*>(&R.phi8);
   const int4 cl = *reinterpret_cast<const int4*>(&R.col[0]);
+  const bool fast = cl.w != 0;
   const double phi8 = ph.x;
   const double w0 = wa.x, w1 = wa.y, w2 = wb.x, w3 = wb.y, w4 = wc.x, w5 = wc.y;
   const int l2 = 2 * s8;
@@ -977,6 +978,10 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
       __syncwarp();
     }
     unsigned n_eval = 0, n_act_row = 0;
+    // point_kernel8 path: points listed but not yet evaluated (they wait for a
+    // full group of four: a warp iteration costs the same with idle segments)
+    constexpr bool kCarry = UWB_SEG8 && HOIST && !MIXED;
+    int n_pend = 0;
     double row_acc = 0.0;
     // Symmetric rows (quadrants 1 and 3: s1 == s2, b1 == b2): u2 -> -u2 swaps f1 and f2,
     // and the integrand is symmetric in them (phase_mismatch is bit-exactly
@@ -1022,6 +1027,7 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
       const unsigned am = __ballot_sync(kFull, active);
       // a mirror column evaluates its own |K|^2 only if its partner is inactive
       const bool partner_active = sym && ((am >> (lane ^ 16)) & 1u);
+      const double pw_partner = __shfl_xor_sync(kFull, pw, 16);
       const bool need = active && (primary || !partner_active);
       const unsigned nm = __ballot_sync(kFull, need);
       const unsigned fm = __ballot_sync(kFull, need && fast);
@@ -1031,14 +1037,21 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
         // fast points first, then slow ones, so half-warp pairs rarely diverge.
         // Column i0 + 1 is always read: clamped stencils have hw1 = 0 and the
         // table carries a zero pad column n.
-        const int pos = fast ? __popc(fm & lt) : __popc(fm) + __popc(sm & lt);
-        UWB_BOUND(pos >= 0 && pos < 32);
+        const int pos = (kCarry ? n_pend : 0) +
+                        (fast ? __popc(fm & lt) : __popc(fm) + __popc(sm & lt));
+        UWB_BOUND(pos >= 0 && pos < 36);
         UWB_BOUND(st1.i1 <= P.n_ch && st2.i1 <= P.n_ch && st3.i1 <= P.n_ch);
         PointRec& R = S.pt[pos];
         R.col[0] = st1.i0 * NS;
         R.col[1] = st2.i0 * NS;
         R.col[2] = st3.i0 * NS;
-        R.src = lane;
+        if (kCarry) {
+          R.src = fast ? 1 : 0;
+          // this column's weight plus its mirror's when the mirror shares |K|^2
+          R.pws = pw + ((sym && primary && partner_active) ? pw_partner : 0.0);
+        } else {
+          R.src = lane;
+        }
         R.w[0] = st1.hw0 * 16.0; R.w[1] = st1.hw1 * 16.0;
         R.w[2] = st2.hw0 * 16.0; R.w[3] = st2.hw1 * 16.0;
         R.w[4] = st3.hw0 * 16.0; R.w[5] = st3.hw1 * 16.0;
@@ -1054,16 +1067,34 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
       n_act_row += __popc(am);
       // warp-uniform trip count: with an odd count the idle half-warp repeats
       // its partner's point (same branch, result dropped) instead of diverging
-      if constexpr (UWB_SEG8 && HOIST && !MIXED) {
-        // four points per warp, one per 8-lane segment (idle segments repeat
-        // point `base`, result dropped)
+      if constexpr (kCarry) {
+        // four points per warp, one per 8-lane segment, in full groups only;
+        // the rest (at most three) move to the front and wait for the next
+        // chunk.  Row sum (gn_integral.hpp:288-305): each group's four
+        // weighted |K|^2 by a fixed tree, groups added in order -- the order
+        // depends on the row's activity pattern only, so rows are
+        // reproducible and independent of scheduling and partitioning.
         const int sg = lane >> 3, s8 = lane & 7;
-        for (int base = 0; base < n_need; base += 4) {
-          const bool ok = base + sg < n_need;
-          const int idx = ok ? base + sg : base;
-          const double kv = point_kernel8<K, FULL, TINY>(P, S, idx, s8, idx < n_fast, z0zero, s_tabs);
-          if (ok && s8 == 0) S.kv[S.pt[idx].src] = kv;
+        const int avail = n_pend + n_need;
+        const int full4 = avail & ~3;
+        for (int base = 0; base < full4; base += 4) {
+          const int idx = base + sg;
+          const double kv = point_kernel8<K, FULL, TINY>(P, S, idx, s8, z0zero, s_tabs);
+          double v = s8 == 0 ? S.pt[idx].pws * kv : 0.0;
+          v += __shfl_xor_sync(kFull, v, 8);
+          v += __shfl_xor_sync(kFull, v, 16);
+          row_acc += v;
         }
+        __syncwarp();
+        n_pend = avail - full4;
+        if (full4 > 0 && n_pend > 0) {  // source [full4, avail) and target [0, n_pend) are disjoint
+          double* d = reinterpret_cast<double*>(S.pt);
+          const double* src = reinterpret_cast<const double*>(S.pt + full4);
+          constexpr int kWords = static_cast<int>(sizeof(PointRec) / sizeof(double));
+          for (int t = lane; t < n_pend * kWords; t += 32) d[t] = src[t];
+        }
+        __syncwarp();
+        continue;
       } else {
         for (int base = 0; base < n_need; base += 2) {
           const bool ok = base + seg < n_need;
@@ -1089,10 +1120,19 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
       row_acc += v;
       __syncwarp();
     }
-    // row sum (gn_integral.hpp:288-305): lane l adds the contiguous run of
-    // columns [l c, (l + 1) c) in ascending j, then a fixed xor tree; the
-    // order depends on (n_r) only, so rows are reproducible and independent
-    // of scheduling and partitioning
+    if constexpr (kCarry) {
+      if (n_pend > 0) {  // the row's last (at most three) points; idle segments repeat point 0
+        const int sg = lane >> 3, s8 = lane & 7;
+        const bool ok = sg < n_pend;
+        const int idx = ok ? sg : 0;
+        const double kv = point_kernel8<K, FULL, TINY>(P, S, idx, s8, z0zero, s_tabs);
+        double v = (ok && s8 == 0) ? S.pt[idx].pws * kv : 0.0;
+        v += __shfl_xor_sync(kFull, v, 8);
+        v += __shfl_xor_sync(kFull, v, 16);
+        row_acc += v;
+        __syncwarp();
+      }
+    }
     if (lane == 0) {
       UWB_BOUND(row < P.total_rows);
       P.rowsum[row] = row_acc * du1 * S.du2;
