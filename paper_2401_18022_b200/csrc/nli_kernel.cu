@@ -222,12 +222,12 @@ __shared__ double2 s_cs16[16];
 //   e2c[j]:  2^(j/16) with j << 16 subtracted from its high word, so that adding
 //            k << 16 (k = 16 e + j) to it yields 2^(k/16) exactly: the exponent
 //            insertion is one shift-add (LEA) instead of shift, mask and add.
+// Each table is its own kernel-scope __shared__ array (StepTabs holds their
+// addresses), so a lookup is [index + uniform base] with no per-lookup base add.
 struct StepTabs {
-  double2 cs16[16];
-  double e2c[16];
-#if UWB_Z_SMEM
-  double z[128];  // the span's end-edge positions (HOIST, K <= 8), lane order
-#endif
+  double2* cs16;  // [16]
+  double* e2c;    // [16]
+  double* z;      // [128] the span's end-edge positions (HOIST, K <= 8), lane order
 };
 
 __device__ __forceinline__ double* S_h(WarpSmem& S) {
@@ -247,7 +247,7 @@ __device__ __forceinline__ double TB_z(const T& tb, int i) {
 #endif
 }
 
-__device__ __forceinline__ void init_step_tabs(StepTabs& T, int i) {
+__device__ __forceinline__ void init_step_tabs(const StepTabs& T, int i) {
   if (i < 16) {
     T.cs16[i] = make_double2(c_tab_cos16[i], c_tab_sin16[i]);
     const double v = c_exp2_tab16[i];
@@ -857,7 +857,10 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
     nli_rows_kernel(const NliParams P) {
   constexpr int kWarps = WarpsFor<HOIST, MIXED>::value;
   __shared__ WarpSmem s_w[kWarps];
-  __shared__ StepTabs s_tabs;
+  __shared__ double2 s_tab_cs16[16];
+  __shared__ double s_tab_e2c[16];
+  __shared__ __align__(16) double s_tab_z[UWB_Z_SMEM ? 128 : 1];
+  const StepTabs s_tabs{s_tab_cs16, s_tab_e2c, s_tab_z};
   init_step_tabs(s_tabs, threadIdx.x);
   if (threadIdx.x < 16) {
     s_exp2_tab[threadIdx.x] = c_exp2_tab16[threadIdx.x];
