@@ -921,49 +921,25 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
     const int n_r = P.n_r;
     double du1;
     {
+      // the row's u1 bin and u2 range, precomputed by row_params_kernel (the
+      // same arithmetic, one thread per row instead of every lane of a warp)
+      const double2 rp0 = __ldg(reinterpret_cast<const double2*>(P.rowpar) + 2 * row);
+      const double2 rp1 = __ldg(reinterpret_cast<const double2*>(P.rowpar) + 2 * row + 1);
+      const double su = rp0.x;
+      if (!(su >= 0.0)) {  // quadrant collapsed or empty u2 range: the reference `continue`s
+        if (lane == 0) {
+          P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
+          P.rowcnt[row] = make_uint2(0u, 0u);
+        }
+        continue;
+      }
+      du1 = __ldg(P.rowsum + row);  // parked there by row_params_kernel
       const int rem = row - probe * per_probe;
       const int q = rem / n_r + 1;
-      const int i = rem - (q - 1) * n_r;
       const double nu = __ldg(P.probe_nu + probe);
       const double f = nu - P.centre;
-      // quadrant_limits (gn_integral.hpp:63-79)
-      const double bm = P.half_band - f, bp = P.half_band + f;
-      double b1, b2, s1, s2;
-      switch (q) {
-        case 1: b1 = bm; b2 = bm; s1 = 1.0; s2 = 1.0; break;
-        case 2: b1 = bp; b2 = bm; s1 = -1.0; s2 = 1.0; break;
-        case 3: b1 = bp; b2 = bp; s1 = -1.0; s2 = -1.0; break;
-        default: b1 = bm; b2 = bp; s1 = 1.0; s2 = -1.0; break;
-      }
-      const double u1_max = b1 * b2;
-      if (!(u1_max > 0.0)) {
-        if (lane == 0) {
-          P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
-          P.rowcnt[row] = make_uint2(0u, 0u);
-        }
-        continue;
-      }
-      // u1 bin (gn_integral.hpp:262-286)
-      double e0, e1;
-      if (P.u1_uniform) {
-        e0 = u1_max * static_cast<double>(i) / n_r;
-        e1 = u1_max * static_cast<double>(i + 1) / n_r;
-      } else {
-        e0 = i == 0 ? 0.0 : u1_max * exp(P.ln_min * static_cast<double>(n_r - i) / (n_r - 1));
-        e1 = u1_max * exp(P.ln_min * static_cast<double>(n_r - i - 1) / (n_r - 1));
-      }
-      du1 = e1 - e0;
-      const double u1 = (e0 == 0.0 || P.u1_uniform) ? 0.5 * (e0 + e1) : sqrt(e0 * e1);
-      const double su = sqrt(u1);
-      const double hi = log(b1 / su);
-      const double lo = -log(b2 / su);
-      if (!(hi > lo)) {
-        if (lane == 0) {
-          P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
-          P.rowcnt[row] = make_uint2(0u, 0u);
-        }
-        continue;
-      }
+      const double s1 = (q == 1 || q == 4) ? 1.0 : -1.0;
+      const double s2 = (q == 1 || q == 2) ? 1.0 : -1.0;
       __syncwarp();
       if (lane == 0) {
         S.nu = nu;
@@ -971,11 +947,13 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
         S.s1 = s1;
         S.s2 = s2;
         S.su = su;
-        S.u1 = u1;
-        S.lo = lo;
-        S.du2 = (hi - lo) / n_r;
+        S.u1 = rp0.y;
+        S.lo = rp1.x;
+        S.du2 = rp1.y;
         // quadrants 1 and 3 (s1 == s2, b1 == b2); quadrant 2 at f = 0 has
         // b1 == b2 too but maps (f1, f2) -> (-f2, -f1): not a symmetry
+        const double bm = P.half_band - f, bp = P.half_band + f;
+        const double b1 = (q == 1 || q == 4) ? bm : bp, b2 = (q == 1 || q == 2) ? bm : bp;
         S.sym = (P.mirror_u2 && s1 == s2 && b1 == b2) ? 1 : 0;
       }
       __syncwarp();
@@ -1144,6 +1122,58 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
     __syncwarp();
 
   }
+}
+
+// Per-row parameters of the hyperbolic grid (gn_integral.hpp:258-286): the u1
+// bin (log or uniform edges), su = sqrt(u1) and the u2 range, one thread per
+// row with exactly the arithmetic the row kernel used to repeat in every lane.
+// rowpar[row] = (su, u1, lo, du2); du1 is parked in rowsum[row] (the row
+// kernel overwrites it with the row's sum).  su = -1 marks a skipped row.
+__global__ void row_params_kernel(const NliParams P) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= P.total_rows) return;
+  const int n_r = P.n_r;
+  const int per_probe = P.n_q * n_r;
+  const int probe = row / per_probe;
+  const int rem = row - probe * per_probe;
+  const int q = rem / n_r + 1;
+  const int i = rem - (q - 1) * n_r;
+  const double nu = P.probe_nu[probe];
+  const double f = nu - P.centre;
+  // quadrant_limits (gn_integral.hpp:63-79)
+  const double bm = P.half_band - f, bp = P.half_band + f;
+  double b1, b2;
+  switch (q) {
+    case 1: b1 = bm; b2 = bm; break;
+    case 2: b1 = bp; b2 = bm; break;
+    case 3: b1 = bp; b2 = bp; break;
+    default: b1 = bm; b2 = bp; break;
+  }
+  double2* rp = reinterpret_cast<double2*>(P.rowpar) + 2 * row;
+  const double u1_max = b1 * b2;
+  if (!(u1_max > 0.0)) {
+    rp[0] = make_double2(-1.0, 0.0);
+    return;
+  }
+  double e0, e1;
+  if (P.u1_uniform) {
+    e0 = u1_max * static_cast<double>(i) / n_r;
+    e1 = u1_max * static_cast<double>(i + 1) / n_r;
+  } else {
+    e0 = i == 0 ? 0.0 : u1_max * exp(P.ln_min * static_cast<double>(n_r - i) / (n_r - 1));
+    e1 = u1_max * exp(P.ln_min * static_cast<double>(n_r - i - 1) / (n_r - 1));
+  }
+  const double u1 = (e0 == 0.0 || P.u1_uniform) ? 0.5 * (e0 + e1) : sqrt(e0 * e1);
+  const double su = sqrt(u1);
+  const double hi = log(b1 / su);
+  const double lo = -log(b2 / su);
+  if (!(hi > lo)) {
+    rp[0] = make_double2(-1.0, 0.0);
+    return;
+  }
+  rp[0] = make_double2(su, u1);
+  rp[1] = make_double2(lo, (hi - lo) / n_r);
+  P.rowsum[row] = e1 - e0;
 }
 
 // Probe half-log columns (gn_integral.hpp:234-251), in log2 units, plus the
@@ -1466,7 +1496,8 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
   cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), stream);
   cudaMemsetAsync(p.n_eval, 0, 2 * sizeof(unsigned long long), stream);  // n_eval, n_active
   probe_halflog_kernel<<<p.n_probes, 128, 0, stream>>>(p);
-  ++launches;
+  row_params_kernel<<<(p.total_rows + 255) / 256, 256, 0, stream>>>(p);
+  launches += 2;
   if (ev_k0) cudaEventRecord(ev_k0, stream);
   static const bool no_co = [] {  // UWB_NLI_NO_CO=1: ignore coresident_smem (A/B)
     const char* e = std::getenv("UWB_NLI_NO_CO");

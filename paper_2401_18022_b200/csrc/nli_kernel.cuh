@@ -67,6 +67,8 @@ struct NliParams {
   int mirror_u2;                // share |K|^2 across u2 -> -u2 in symmetric rows
   int mixed;                    // 1: compensated-FP32 step arithmetic (uwb_set_precision)
   double* rowsum;               // [total_rows]; NaN => row not added (reference `continue`)
+  double* rowpar;               // [total_rows][4] su, u1, lo, du2 (+ du1 in rowsum until the
+                                // row is done); su < 0: the row is skipped (row_params_kernel)
 };
 
 struct FinalizeParams {

@@ -233,6 +233,7 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
   P.probe_nu = d_nu;
   P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * P.col_stride);
   P.rowsum = c->rowsum.get<double>(std::max(P.total_rows, 1));
+  P.rowpar = c->rowpar.get<double>(4 * static_cast<size_t>(std::max(P.total_rows, 1)));
   P.counter = c->counter.get<unsigned int>(1);
   P.n_eval = c->n_eval.get<unsigned long long>(2);
   P.n_active = P.n_eval + 1;
@@ -241,7 +242,7 @@ int run_probes(uwb_ctx* c, NliParams& P, const uwb_nli_cfg* cfg, const std::vect
   F.probe_gamma = d_g;
   F.probe_g = c->probe_g.get<double>(std::max(np, 1));
   F.probe_quad = c->probe_quad.get<double>(4 * std::max(np, 1));
-  if (!P.hl2 || !P.rowsum || !P.counter || !F.probe_g || !F.probe_quad || !d_nu || !d_g)
+  if (!P.hl2 || !P.rowsum || !P.rowpar || !P.counter || !F.probe_g || !F.probe_quad || !d_nu || !d_g)
     return fail(UWB_CUDA_ERROR, "device allocation failed");
   cudaStream_t st = c->stream;
   if (np) {
@@ -398,7 +399,7 @@ void uwb_ctx_destroy(uwb_ctx* c) {
   c->bsubs.clear();
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   for (DBuf* b : {&c->freq, &c->psd, &c->gamma, &c->log2rho, &c->zedge, &c->zstart, &c->zmid, &c->width,
-                  &c->wlast, &c->span_steps, &c->probe_nu, &c->probe_chan, &c->probe_work, &c->rowcnt, &c->probe_gamma, &c->hl2, &c->rowsum, &c->counter,
+                  &c->wlast, &c->span_steps, &c->probe_nu, &c->probe_chan, &c->probe_work, &c->rowcnt, &c->probe_gamma, &c->hl2, &c->rowsum, &c->rowpar, &c->counter,
                   &c->n_eval, &c->probe_g, &c->probe_quad, &c->chan_probe0, &c->eta, &c->nli_psd,
                   &c->nli_power, &c->quad, &c->skipped, &c->batch_psd, &c->batch_report, &c->batch_ode, &c->alpha, &c->aeff, &c->raman_x,
                   &c->raman_y, &c->nf_db, &c->guard, &c->rho_end, &c->ode_work, &c->ode_gwork, &c->report,

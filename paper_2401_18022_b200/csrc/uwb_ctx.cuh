@@ -61,7 +61,8 @@ struct uwb_ctx {
   // probes + work
   uwb::DBuf probe_work;  // per-probe |K|^2 evaluations of the last NLI
   uwb::DBuf rowcnt;      // per-row work counts (summed per probe by the finalize)
-  uwb::DBuf probe_nu, probe_chan, probe_gamma, hl2, rowsum, counter, n_eval, probe_g, probe_quad, chan_probe0;
+  uwb::DBuf probe_nu, probe_chan, probe_gamma, hl2, rowsum, rowpar, counter, n_eval, probe_g, probe_quad,
+      chan_probe0;
   // per-channel results
   uwb::DBuf eta, nli_psd, nli_power, quad, skipped;
   // uwb_evaluate_link_many: the batch's launch profiles and reports

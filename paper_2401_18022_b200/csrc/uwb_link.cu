@@ -288,6 +288,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   P.probe_chan = up(c, c->probe_chan, pch.data(), pch.size());
   P.hl2 = c->hl2.get<double>(static_cast<size_t>(std::max(np, 1)) * P.n_spans * NS);
   P.rowsum = c->rowsum.get<double>(std::max(P.total_rows, 1));
+  P.rowpar = c->rowpar.get<double>(4 * static_cast<size_t>(std::max(P.total_rows, 1)));
   P.counter = c->counter.get<unsigned int>(1);
   P.n_eval = c->n_eval.get<unsigned long long>(2);
   P.n_active = P.n_eval + 1;
@@ -374,7 +375,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
   pr->grid_ctas = c->sm_count * per_sm;
   if (!P.log2rho || !P.zedge || !P.zstart || !P.zmid || !P.width || !P.wlast || !P.probe_nu ||
-      !P.probe_chan || !P.hl2 || !P.rowsum || !P.counter || !P.n_eval || !P.probe_work || !P.rowcnt ||
+      !P.probe_chan || !P.hl2 || !P.rowsum || !P.rowpar || !P.counter || !P.n_eval || !P.probe_work || !P.rowcnt ||
       !F.probe_gamma ||
       !F.probe_g || !F.probe_quad || !F.chan_probe0 || !F.eta || !F.nli_psd || !F.nli_power ||
       !F.quad || !F.skipped || !L.out || !d_freq || !pr->d_psd || !d_guard || !d_alpha ||

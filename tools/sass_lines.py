@@ -25,7 +25,7 @@ for l in txt[start + 1:]:
     if m:
         cur = (m.group(1).split("/")[-1], int(m.group(2)))
         continue
-    if re.match(r"\s*/\*[0-9a-f]{4}\*/", l):
+    if re.match(r"\s*/\*[0-9a-f]{4,6}\*/", l):
         idx2.append(cur)
 rows = list(csv.reader(open(sass_csv)))
 h = rows[1]
