@@ -526,9 +526,9 @@ int uwb_evaluate_link_many(uwb_ctx* c, int n_eval, const double* psd_host, doubl
     // its own stream) runs while the integrand of evaluation e occupies the
     // other SMs.  Two ODE output buffers alternate; the integrand grid leaves
     // one SM's worth of CTAs free, and the ODE runs its 224-register build
-    // (7,168 registers per warp: it fits in an SM sub-partition beside three
-    // 96-register integrand warps), so it finds room wherever the integrand's
-    // CTAs were placed; the integrand's carveout leaves it shared memory.
+    // (7,168 registers per warp: it fits in an SM sub-partition beside one
+    // integrand CTA's warps), so it finds room wherever the integrand's CTAs
+    // were placed; the integrand's carveout leaves it shared memory.
     int rc = ensure_batch_state(c);
     if (rc) return rc;
     uwb_ctx::BatchState& B = *c->batch;
