@@ -399,13 +399,14 @@ void uwb_ctx_destroy(uwb_ctx* c) {
   c->bsubs.clear();
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   for (DBuf* b : {&c->freq, &c->psd, &c->gamma, &c->log2rho, &c->zedge, &c->zstart, &c->zmid, &c->width,
-                  &c->wlast, &c->span_steps, &c->probe_nu, &c->probe_chan, &c->probe_work, &c->rowcnt, &c->probe_gamma, &c->hl2, &c->rowsum, &c->rowpar, &c->counter,
+                  &c->wlast, &c->span_steps, &c->probe_nu, &c->probe_chan, &c->probe_work, &c->rowcnt, &c->probe_gamma, &c->hl2, &c->rowsum, &c->rowpar, &c->up_dev, &c->counter,
                   &c->n_eval, &c->probe_g, &c->probe_quad, &c->chan_probe0, &c->eta, &c->nli_psd,
                   &c->nli_power, &c->quad, &c->skipped, &c->batch_psd, &c->batch_report, &c->batch_ode, &c->alpha, &c->aeff, &c->raman_x,
                   &c->raman_y, &c->nf_db, &c->guard, &c->rho_end, &c->ode_work, &c->ode_gwork, &c->report,
                   &c->mid, &c->edge})
     b->release();
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->up_pinned) cudaFreeHost(c->up_pinned);
   if (c->batch) {
     for (cudaEvent_t ev : {c->batch->ev_start, c->batch->ev_ode[0], c->batch->ev_ode[1],
                            c->batch->ev_nli[0], c->batch->ev_nli[1]})

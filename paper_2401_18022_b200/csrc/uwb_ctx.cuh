@@ -89,6 +89,19 @@ struct uwb_ctx {
   // pinned host staging for small transfers
   void* pinned = nullptr;
   size_t pinned_cap = 0;
+  // deferred uploads (evaluate_link prepare): the host arrays are packed into
+  // one staging block, copied with ONE host-to-device transfer and scattered to
+  // their buffers by one kernel, instead of ~20 pageable cudaMemcpyAsync calls
+  struct UpSeg {
+    void* dst;
+    size_t off, bytes;
+  };
+  bool up_defer = false;
+  std::vector<unsigned char> up_host;
+  std::vector<UpSeg> up_segs;
+  void* up_pinned = nullptr;
+  size_t up_pinned_cap = 0;
+  uwb::DBuf up_dev;
   // probes of the last NLI: first probe of each channel (-1: none) and
   // probes per channel (3 with Simpson), for uwb_last_channel_work
   std::vector<int> last_chan_probe0;

@@ -165,12 +165,101 @@ int distance_grid_host(double length_m, double density, std::vector<double>* edg
 
 namespace {
 
+// Host-to-device copy of n elements into the buffer b; while the context
+// defers uploads (prepare) the bytes are staged and go with the next flush.
+void stage_upload(uwb_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (!c->up_defer) {
+    xfer(c, dst, src, bytes, cudaMemcpyHostToDevice, c->stream);
+    return;
+  }
+  const size_t off = (c->up_host.size() + 15) & ~static_cast<size_t>(15);
+  c->up_host.resize(off + bytes);
+  std::memcpy(c->up_host.data() + off, src, bytes);
+  c->up_segs.push_back({dst, off, bytes});
+}
+
 template <class T>
 T* up(uwb_ctx* c, DBuf& b, const T* src, size_t n) {
   T* d = b.get<T>(std::max<size_t>(n, 1));
-  if (d && src && n) xfer(c, d, src, n * sizeof(T), cudaMemcpyHostToDevice, c->stream);
+  if (d && src && n) stage_upload(c, d, src, n * sizeof(T));
   return d;
 }
+
+constexpr int kMaxScatter = 32;
+struct ScatterDesc {
+  int n;
+  unsigned char* dst[kMaxScatter];
+  unsigned off[kMaxScatter];
+  unsigned bytes[kMaxScatter];
+};
+
+// one CTA per staged segment: 8-byte words where both ends are aligned (every
+// double / int array), bytes otherwise (the guard flags)
+__global__ void scatter_uploads_kernel(const unsigned char* src, ScatterDesc d) {
+  const int s = blockIdx.x;
+  if (s >= d.n) return;
+  unsigned char* dst = d.dst[s];
+  const unsigned char* p = src + d.off[s];
+  const unsigned nb = d.bytes[s];
+  if (((reinterpret_cast<uintptr_t>(dst) | d.off[s] | nb) & 7u) == 0) {
+    for (unsigned i = threadIdx.x; i < nb / 8; i += blockDim.x)
+      reinterpret_cast<unsigned long long*>(dst)[i] = reinterpret_cast<const unsigned long long*>(p)[i];
+  } else {
+    for (unsigned i = threadIdx.x; i < nb; i += blockDim.x) dst[i] = p[i];
+  }
+}
+
+// Issue the staged uploads: one pinned host-to-device copy, one scatter launch
+// per 32 segments.  Clears the staging and the deferral.
+int flush_uploads(uwb_ctx* c) {
+  c->up_defer = false;
+  const size_t total = c->up_host.size();
+  int rc = UWB_OK;
+  if (total) {
+    if (c->up_pinned_cap < total) {
+      if (c->up_pinned) cudaFreeHost(c->up_pinned);
+      c->up_pinned = nullptr;
+      c->up_pinned_cap = 0;
+      if (cudaMallocHost(&c->up_pinned, total) != cudaSuccess) rc = fail(UWB_CUDA_ERROR, "pinned alloc");
+      else c->up_pinned_cap = total;
+    }
+    unsigned char* dev = c->up_dev.get<unsigned char>(total);
+    if (!rc && !dev) rc = fail(UWB_CUDA_ERROR, "device allocation failed");
+    if (!rc) {
+      std::memcpy(c->up_pinned, c->up_host.data(), total);
+      xfer(c, dev, c->up_pinned, total, cudaMemcpyHostToDevice, c->stream);
+      for (size_t b = 0; b < c->up_segs.size(); b += kMaxScatter) {
+        ScatterDesc d{};
+        d.n = static_cast<int>(std::min<size_t>(kMaxScatter, c->up_segs.size() - b));
+        for (int k = 0; k < d.n; ++k) {
+          const uwb_ctx::UpSeg& u = c->up_segs[b + k];
+          d.dst[k] = static_cast<unsigned char*>(u.dst);
+          d.off[k] = static_cast<unsigned>(u.off);
+          d.bytes[k] = static_cast<unsigned>(u.bytes);
+        }
+        scatter_uploads_kernel<<<d.n, 128, 0, c->stream>>>(dev, d);
+      }
+    }
+  }
+  c->up_host.clear();
+  c->up_segs.clear();
+  return rc;
+}
+
+// Defers the context's uploads for a scope; an early return drops them.
+struct UploadBatch {
+  uwb_ctx* c;
+  explicit UploadBatch(uwb_ctx* cc) : c(cc) {
+    c->up_defer = true;
+    c->up_host.clear();
+    c->up_segs.clear();
+  }
+  ~UploadBatch() {
+    c->up_defer = false;
+    c->up_host.clear();
+    c->up_segs.clear();
+  }
+};
 
 }  // namespace
 
@@ -187,7 +276,8 @@ void release_link_state(uwb_ctx* c) {
 }
 
 int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_cfg* lk,
-            const uwb_nli_cfg* cfg) {
+            const uwb_nli_cfg* cfg, bool sync) {
+  UploadBatch uploads(c);  // every host array of the link goes with one transfer
   // the buffers below are shared with the previous prepared link: it is gone
   // from here on, and the new one is published only once complete
   release_link_state(c);
@@ -351,7 +441,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   O.rho_end = d_rho_end;
   O.status = pr->d_status;
   O.rhs_evals = pr->d_rhs;
-  xfer(c, d_band2, band.data(), n * sizeof(int), cudaMemcpyHostToDevice, c->stream);
+  stage_upload(c, d_band2, band.data(), n * sizeof(int));
 
   // assembly
   LinkDev& L = pr->L;
@@ -381,7 +471,8 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
       !F.quad || !F.skipped || !L.out || !d_freq || !pr->d_psd || !d_guard || !d_alpha ||
       !pr->d_aeff || !d_nf || !d_mid)
     return fail(UWB_CUDA_ERROR, "device allocation failed");
-  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if ((rc = flush_uploads(c))) return rc;
+  cudaError_t e = sync ? cudaStreamSynchronize(c->stream) : cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "prepare");
   c->prep = owner.release();  // complete: publish
   return UWB_OK;
@@ -604,7 +695,7 @@ int uwb_evaluate_link(uwb_ctx* c, const uwb_grid* grid, const uwb_fibre* fibre,
   if (c->multi()) return multi_evaluate_link(c, grid, fibre, link, cfg, out);
   cudaSetDevice(c->device);
   reset_xfer(c);
-  int rc = prepare(c, grid, fibre, link, cfg);
+  int rc = prepare(c, grid, fibre, link, cfg, /*sync=*/false);  // same stream throughout
   if (rc) return rc;
   uwb_ctx::Prepared* pr = c->prep;
   if ((rc = run_prepared(c, nullptr, c->stream))) return rc;

@@ -60,8 +60,11 @@ struct uwb_ctx::Prepared {
 namespace uwb {
 
 // evaluate_link's stages on a prepared context (uwb_link.cu).
+// sync = false only when everything that reads the prepared state runs on the
+// context's own stream (uwb_evaluate_link); the public prepare synchronises so
+// resident calls may use any stream.
 int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_cfg* lk,
-            const uwb_nli_cfg* cfg);
+            const uwb_nli_cfg* cfg, bool sync = true);
 // solve_link_noise (link_optimizer.hpp:181-190): Raman ODE + NLI of the
 // context's channels; psd_dev = launch PSD on the device, or null for the
 // prepared one.
