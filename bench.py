@@ -498,7 +498,7 @@ def run_engine(args):
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if achieved else None,
                          "traffic": tr.get("dram_bytes_per_launch") if tr else None,
-                         "kernel": "nli_rows_kernel (GN integrand)",
+                         "kernel": "nli_list_kernel (GN integrand; the point setup runs in nli_setup_kernel beside the Raman ODE)",
                          "kernel_ms": kmax, "inner_steps": inner,
                          "inner_steps_reference": inner_ref,
                          "effective_tflops_reference_steps": effective,

@@ -1124,6 +1124,199 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
   }
 }
 
+// ---- split evaluation (launch_nli_setup / launch_nli_lists) ----------------
+// Pass 1 (nli_setup_kernel, beside the Raman ODE): every row's column setup
+// (coordinates, the three PSD windows and stencils, phi, the mirror sharing),
+// compacted exactly like the fused kernel's chunks, written as point records
+// to the row's slot list.  Pass 2 (nli_list_kernel): the fused kernel's group
+// loop over the listed records.  Both keep the fused order, so the row sums
+// are bit-identical to nli_rows_kernel's.
+constexpr int kSetupWarps = 8;
+
+__global__ void __launch_bounds__(kSetupWarps * 32) nli_setup_kernel(const NliParams P) {
+  if (threadIdx.x < 16) s_exp2_tab[threadIdx.x] = c_exp2_tab16[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int NS = P.col_stride;
+  const int n_r = P.n_r;
+  const int per_probe = P.n_q * n_r;
+  for (;;) {
+    int row = 0;
+    if (lane == 0) row = static_cast<int>(atomicAdd(P.counter, 1u));
+    row = __shfl_sync(kFull, row, 0);
+    if (row >= P.total_rows) break;
+    const int probe = row / per_probe;
+    const double2 rp0 = __ldg(reinterpret_cast<const double2*>(P.rowpar) + 2 * row);
+    const double2 rp1 = __ldg(reinterpret_cast<const double2*>(P.rowpar) + 2 * row + 1);
+    const bool dark = P.probe_chan && !(__ldg(P.psd + __ldg(P.probe_chan + probe)) > 0.0);
+    if (dark || !(rp0.x >= 0.0)) {  // the reference `continue`s (gn_integral.hpp:349-352, :283)
+      if (lane == 0) {
+        P.rowsum[row] = __longlong_as_double(0x7ff8000000000000ll);
+        P.rowcnt[row] = make_uint2(0u, 0u);
+        P.plist_n[row] = -1;
+      }
+      continue;
+    }
+    const int rem = row - probe * per_probe;
+    const int q = rem / n_r + 1;
+    const double nu = __ldg(P.probe_nu + probe);
+    const double f = nu - P.centre;
+    const double s1 = (q == 1 || q == 4) ? 1.0 : -1.0;
+    const double s2 = (q == 1 || q == 2) ? 1.0 : -1.0;
+    const double bm = P.half_band - f, bp = P.half_band + f;
+    const double b1 = (q == 1 || q == 4) ? bm : bp, b2 = (q == 1 || q == 2) ? bm : bp;
+    const bool sym = P.mirror_u2 && s1 == s2 && b1 == b2;
+    const double su = rp0.x, u1 = rp0.y, lo = rp1.x, du2 = rp1.y;
+    PointRec* out = static_cast<PointRec*>(P.plist) + static_cast<size_t>(row) * n_r;
+    int count = 0;
+    unsigned n_eval = 0, n_act_row = 0;
+    const int half = sym ? (n_r + 1) / 2 : n_r;
+    const int span = sym ? 16 : 32;
+    for (int jb = 0; jb < half; jb += span) {
+      // the fused kernel's column setup (nli_rows_kernel, gn_integral.hpp:288-303)
+      const int m = sym ? jb + (lane & 15) : jb + lane;
+      const bool primary = !sym || lane < 16;
+      const int j = primary ? m : n_r - 1 - m;
+      const bool valid = m < half && (primary || j != m);
+      bool active = false;
+      bool fast = false;
+      Stencil st1, st2, st3;
+      double phi = 0.0, pw = 0.0;
+      if (valid) {
+        const double u2 = lo + (static_cast<double>(j) + 0.5) * du2;
+        const double g1 = su * dev_exp2_16(u2 * (16.0 * kLog2e));
+        const double g2 = u1 * __drcp_rn(g1);
+        const double f1 = s1 * g1;
+        const double f2 = s2 * g2;
+        double p1, p2, p3;
+        st1 = psd_and_stencil(P, nu + f1, &p1);
+        st2 = psd_and_stencil(P, nu + f2, &p2);
+        st3 = psd_and_stencil(P, nu + f1 + f2, &p3);
+        active = p1 != 0.0 && p2 != 0.0 && p3 != 0.0;
+        if (active) {
+          phi = phase_mismatch(f1, f2, f, P.beta2, P.beta3, P.beta4);
+          pw = p1 * p2 * p3;
+          fast = fabs(phi) * __ldg(P.wlast) > 1e-4;
+        }
+      }
+      const unsigned am = __ballot_sync(kFull, active);
+      const bool partner_active = sym && ((am >> (lane ^ 16)) & 1u);
+      const double pw_partner = __shfl_xor_sync(kFull, pw, 16);
+      const bool need = active && (primary || !partner_active);
+      const unsigned nm = __ballot_sync(kFull, need);
+      const unsigned fm = __ballot_sync(kFull, need && fast);
+      const unsigned sm = nm & ~fm;
+      const unsigned lt = (1u << lane) - 1u;
+      if (need) {
+        const int pos = count + (fast ? __popc(fm & lt) : __popc(fm) + __popc(sm & lt));
+        UWB_BOUND(pos >= 0 && pos < n_r);
+        const double phi8 = phi * kUnitInv;
+        double2* r2 = reinterpret_cast<double2*>(out + pos);
+        __stcs(r2 + 0, make_double2(st1.hw0 * 16.0, st1.hw1 * 16.0));
+        __stcs(r2 + 1, make_double2(st2.hw0 * 16.0, st2.hw1 * 16.0));
+        __stcs(r2 + 2, make_double2(st3.hw0 * 16.0, st3.hw1 * 16.0));
+        __stcs(r2 + 3, make_double2(phi8, phi != 0.0 ? __drcp_rn(phi8) : 0.0));
+        __stcs(reinterpret_cast<int4*>(r2 + 4),
+               make_int4(st1.i0 * NS, st2.i0 * NS, st3.i0 * NS, fast ? 1 : 0));
+        __stcs(r2 + 5, make_double2(phi, pw + ((sym && primary && partner_active) ? pw_partner : 0.0)));
+      }
+      count += __popc(nm);
+      n_eval += __popc(nm);
+      n_act_row += __popc(am);
+    }
+    if (lane == 0) {
+      P.plist_n[row] = count;
+      P.rowcnt[row] = make_uint2(n_eval, n_act_row);
+    }
+  }
+}
+
+template <int K, bool FULL, bool TINY>
+__global__ void __launch_bounds__(UWB_NLI_WARPS * 32, UWB_NLI_MIN_BLOCKS)
+    nli_list_kernel(const NliParams P) {
+  constexpr int kWarps = UWB_NLI_WARPS;
+  constexpr int NS = 16 * K;
+  __shared__ WarpSmem s_w[kWarps];
+  __shared__ double2 s_tab_cs16[16];
+  __shared__ double s_tab_e2c[16];
+  __shared__ __align__(16) double s_tab_z[128];
+  const StepTabs s_tabs{s_tab_cs16, s_tab_e2c, s_tab_z};
+  init_step_tabs(s_tabs, threadIdx.x);
+  if (threadIdx.x < 16)
+    s_cs16[threadIdx.x] = make_double2(c_tab_cos16[threadIdx.x], c_tab_sin16[threadIdx.x]);
+  if (threadIdx.x < NS) s_tab_z[threadIdx.x] = __ldg(P.zedge + threadIdx.x);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  WarpSmem& S = s_w[threadIdx.x >> 5];
+  const int n_r = P.n_r;
+  const int per_probe = P.n_q * n_r;
+  const bool z0zero = __ldg(P.zstart) == 0.0;
+  int cur_probe = -1;
+  for (;;) {
+    int row = 0;
+    if (lane == 0) row = static_cast<int>(atomicAdd(P.counter, 1u));
+    row = __shfl_sync(kFull, row, 0);
+    if (row >= P.total_rows) break;
+    const int n = __ldg(P.plist_n + row);
+    if (n < 0) continue;  // skipped: the setup pass wrote its NaN and counts
+    const int probe = row / per_probe;
+    if (probe != cur_probe) {
+      cur_probe = probe;
+      __syncwarp();
+      for (int m = lane; m < NS; m += 32) S_h(S)[m] = __ldg(P.hl2 + static_cast<size_t>(probe) * NS + m);
+      __syncwarp();
+    }
+    const double2* src = reinterpret_cast<const double2*>(static_cast<const PointRec*>(P.plist) +
+                                                          static_cast<size_t>(row) * n_r);
+    constexpr int kRec2 = static_cast<int>(sizeof(PointRec) / sizeof(double2));
+    int n_pend = 0;
+    double row_acc = 0.0;
+    const int sg = lane >> 3, s8 = lane & 7;
+    for (int c0 = 0; c0 < n; c0 += 32) {
+      const int cnt = min(32, n - c0);
+      double2* dst = reinterpret_cast<double2*>(S.pt + n_pend);
+      for (int t = lane; t < cnt * kRec2; t += 32) dst[t] = __ldcs(src + c0 * kRec2 + t);
+      __syncwarp();
+      // the fused kernel's groups of four with the remainder carried over
+      const int avail = n_pend + cnt;
+      const int full4 = avail & ~3;
+      for (int base = 0; base < full4; base += 4) {
+        const int idx = base + sg;
+        const double kv = point_kernel8<K, FULL, TINY>(P, S, idx, s8, z0zero, s_tabs);
+        double v = s8 == 0 ? S.pt[idx].pws * kv : 0.0;
+        v += __shfl_xor_sync(kFull, v, 8);
+        v += __shfl_xor_sync(kFull, v, 16);
+        row_acc += v;
+      }
+      __syncwarp();
+      n_pend = avail - full4;
+      if (full4 > 0 && n_pend > 0) {
+        double* d = reinterpret_cast<double*>(S.pt);
+        const double* sp = reinterpret_cast<const double*>(S.pt + full4);
+        constexpr int kWords = static_cast<int>(sizeof(PointRec) / sizeof(double));
+        for (int t = lane; t < n_pend * kWords; t += 32) d[t] = sp[t];
+      }
+      __syncwarp();
+    }
+    if (n_pend > 0) {
+      const bool ok = sg < n_pend;
+      const int idx = ok ? sg : 0;
+      const double kv = point_kernel8<K, FULL, TINY>(P, S, idx, s8, z0zero, s_tabs);
+      double v = (ok && s8 == 0) ? S.pt[idx].pws * kv : 0.0;
+      v += __shfl_xor_sync(kFull, v, 8);
+      v += __shfl_xor_sync(kFull, v, 16);
+      row_acc += v;
+      __syncwarp();
+    }
+    if (lane == 0) {
+      const double du1 = P.rowsum[row];  // parked by row_params_kernel
+      const double du2 = __ldg(P.rowpar + 4 * static_cast<size_t>(row) + 3);
+      P.rowsum[row] = row_acc * du1 * du2;
+    }
+    __syncwarp();
+  }
+}
+
 // Per-row parameters of the hyperbolic grid (gn_integral.hpp:258-286): the u1
 // bin (log or uniform edges), su = sqrt(u1) and the u2 range, one thread per
 // row with exactly the arithmetic the row kernel used to repeat in every lane.
@@ -1482,6 +1675,31 @@ int nli_ctas_per_sm(int steps, bool one_span, int n_r, bool mixed, bool tiny, bo
   return n;
 }
 
+using ListKernel = void (*)(const NliParams);
+
+template <int K>
+ListKernel pick_list(bool full, bool tiny) {
+  if (tiny) return full ? nli_list_kernel<K, true, true> : nli_list_kernel<K, false, true>;
+  return full ? nli_list_kernel<K, true, false> : nli_list_kernel<K, false, false>;
+}
+
+ListKernel list_kernel_for(const NliParams& p) {
+  const int K = (p.steps + 15) / 16;
+  const bool full = p.steps == 16 * K;
+  const bool tiny = p.slow_tiny != 0;
+  switch (K) {
+    case 1: return pick_list<1>(full, tiny);
+    case 2: return pick_list<2>(full, tiny);
+    case 3: return pick_list<3>(full, tiny);
+    case 4: return pick_list<4>(full, tiny);
+    case 5: return pick_list<5>(full, tiny);
+    case 6: return pick_list<6>(full, tiny);
+    case 7: return pick_list<7>(full, tiny);
+    case 8: return pick_list<8>(full, tiny);
+    default: return nullptr;
+  }
+}
+
 int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaStream_t stream,
                cudaEvent_t ev_k0, cudaEvent_t ev_k1, size_t coresident_smem) {
   // UWB_NLI_NO_HOIST=1 selects the per-point z/half-log loads (A/B experiments)
@@ -1505,6 +1723,60 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
   }();
   allow_row_smem(k, p.n_r, no_co ? 0 : coresident_smem);
   k<<<grid_ctas, row_threads(k), row_smem(p.n_r), stream>>>(p);
+  ++launches;
+  if (ev_k1) cudaEventRecord(ev_k1, stream);
+  const size_t fin_smem = static_cast<size_t>(p.n_q) * p.n_r * sizeof(double);
+  if (fin_smem > 48 * 1024)
+    cudaFuncSetAttribute(finalize_probes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(fin_smem));
+  finalize_probes_kernel<<<f.n_probes, 128, fin_smem, stream>>>(p, f);
+  ++launches;
+  if (f.n_ch > 0) {
+    finalize_channels_kernel<<<(f.n_ch + 127) / 128, 128, 0, stream>>>(f);
+    ++launches;
+  }
+  return launches;
+}
+
+bool nli_split_ok(const NliParams& p) {
+  static const bool off = [] {  // UWB_NLI_NO_SPLIT=1: the fused kernel only (A/B)
+    const char* e = std::getenv("UWB_NLI_NO_SPLIT");
+    return e && e[0] == '1';
+  }();
+  return !off && UWB_SEG8 && UWB_Z_SMEM && p.n_spans == 1 && !p.span_steps && !p.mixed &&
+         p.steps >= 1 && p.steps <= 128 && p.col_stride == 16 * ((p.steps + 15) / 16);
+}
+
+size_t nli_point_record_bytes() { return sizeof(PointRec); }
+
+int nli_setup_ctas_per_sm() {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, nli_setup_kernel, kSetupWarps * 32, 0) !=
+      cudaSuccess)
+    return 0;
+  return n;
+}
+
+int launch_nli_setup(const NliParams& p, int grid_ctas, cudaStream_t side) {
+  if (!nli_split_ok(p) || !p.plist || !p.plist_n || p.n_probes <= 0) return -1;
+  cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), side);
+  cudaMemsetAsync(p.n_eval, 0, 2 * sizeof(unsigned long long), side);  // n_eval, n_active
+  row_params_kernel<<<(p.total_rows + 255) / 256, 256, 0, side>>>(p);
+  nli_setup_kernel<<<grid_ctas, kSetupWarps * 32, 0, side>>>(p);
+  cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), side);  // the list pass's queue
+  return 2;
+}
+
+int launch_nli_lists(const NliParams& p, const FinalizeParams& f, int grid_ctas,
+                     cudaStream_t stream, cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
+  ListKernel k = list_kernel_for(p);
+  if (!k) return -1;
+  int launches = 0;
+  probe_halflog_kernel<<<p.n_probes, 128, 0, stream>>>(p);
+  ++launches;
+  if (ev_k0) cudaEventRecord(ev_k0, stream);
+  allow_row_smem(k, p.n_r);  // the same carveout rule as the fused kernel
+  k<<<grid_ctas, UWB_NLI_WARPS * 32, 0, stream>>>(p);
   ++launches;
   if (ev_k1) cudaEventRecord(ev_k1, stream);
   const size_t fin_smem = static_cast<size_t>(p.n_q) * p.n_r * sizeof(double);

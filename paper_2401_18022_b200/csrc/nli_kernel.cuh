@@ -59,6 +59,12 @@ struct NliParams {
   // work queue + outputs
   int total_rows;               // n_probes * n_q * n_r
   unsigned int* counter;        // row queue head (zeroed before launch)
+  // Split evaluation (launch_nli_setup / launch_nli_lists): the rows' point
+  // records written by the setup pass while the Raman ODE runs, [row][n_r]
+  // records of nli_point_record_bytes() each, and each row's record count
+  // (-1: the row is skipped).  Null: the fused kernel.
+  void* plist;
+  int* plist_n;
   unsigned long long* n_eval;   // [2]: |K|^2 evaluations, active points (stats)
   unsigned long long* n_active; // = n_eval + 1
   uint2* rowcnt;                // [total_rows] (|K|^2 evaluations, active points) per row
@@ -126,6 +132,20 @@ inline void append_span_tables(const double* edge, const double* mid, const doub
 // integrand's shared-memory carveout accordingly (0: smallest carveout, most L1).
 int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaStream_t stream,
                cudaEvent_t ev_k0, cudaEvent_t ev_k1, size_t coresident_smem = 0);
+
+// Split evaluation of single-span FP64 problems with K <= 8 (nli_split_ok):
+// launch_nli_setup issues the row parameters and the per-row point records
+// (everything the launch PSD decides; nothing depends on the power profile)
+// on `side`, with `grid_ctas` CTAs -- it runs beside the Raman ODE; then
+// launch_nli_lists evaluates the listed points (probe half-logs, rows,
+// finalize) on `stream` once the ODE and the setup are done.  The row sums
+// are bit-identical to launch_nli's.
+bool nli_split_ok(const NliParams& p);
+size_t nli_point_record_bytes();
+int nli_setup_ctas_per_sm();
+int launch_nli_setup(const NliParams& p, int grid_ctas, cudaStream_t side);
+int launch_nli_lists(const NliParams& p, const FinalizeParams& f, int grid_ctas,
+                     cudaStream_t stream, cudaEvent_t ev_k0, cudaEvent_t ev_k1);
 
 // CTAs per SM the integrand kernel reaches for a given step count.
 int nli_ctas_per_sm(int steps, bool one_span, int n_r, bool mixed = false, bool tiny = false,

@@ -399,7 +399,7 @@ void uwb_ctx_destroy(uwb_ctx* c) {
   c->bsubs.clear();
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   for (DBuf* b : {&c->freq, &c->psd, &c->gamma, &c->log2rho, &c->zedge, &c->zstart, &c->zmid, &c->width,
-                  &c->wlast, &c->span_steps, &c->probe_nu, &c->probe_chan, &c->probe_work, &c->rowcnt, &c->probe_gamma, &c->hl2, &c->rowsum, &c->rowpar, &c->up_dev, &c->counter,
+                  &c->wlast, &c->span_steps, &c->probe_nu, &c->probe_chan, &c->probe_work, &c->rowcnt, &c->probe_gamma, &c->hl2, &c->rowsum, &c->rowpar, &c->up_dev, &c->plist, &c->plist_n, &c->counter,
                   &c->n_eval, &c->probe_g, &c->probe_quad, &c->chan_probe0, &c->eta, &c->nli_psd,
                   &c->nli_power, &c->quad, &c->skipped, &c->batch_psd, &c->batch_report, &c->batch_ode, &c->alpha, &c->aeff, &c->raman_x,
                   &c->raman_y, &c->nf_db, &c->guard, &c->rho_end, &c->ode_work, &c->ode_gwork, &c->report,
@@ -415,8 +415,10 @@ void uwb_ctx_destroy(uwb_ctx* c) {
     delete c->batch;
     c->batch = nullptr;
   }
-  for (cudaEvent_t ev : {c->ev0, c->ev1, c->evk0, c->evk1})
+  if (c->s_setup) cudaStreamSynchronize(c->s_setup);
+  for (cudaEvent_t ev : {c->ev0, c->ev1, c->evk0, c->evk1, c->ev_fork, c->ev_join})
     if (ev) cudaEventDestroy(ev);
+  if (c->s_setup) cudaStreamDestroy(c->s_setup);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }

@@ -74,6 +74,11 @@ struct uwb_ctx {
     cudaEvent_t ev_start = nullptr, ev_ode[2] = {nullptr, nullptr}, ev_nli[2] = {nullptr, nullptr};
   };
   BatchState* batch = nullptr;
+  // split evaluation (launch_nli_setup beside the Raman ODE): per-row point
+  // records and counts, the setup pass's stream and its fork/join events
+  uwb::DBuf plist, plist_n;
+  cudaStream_t s_setup = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // link evaluation state (raman ODE + assembly)
   uwb::DBuf alpha, aeff, raman_x, raman_y, nf_db, guard, rho_end, ode_work, ode_gwork, report, mid, edge;
   std::vector<int> subset;

@@ -464,6 +464,32 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   const int per_sm = nli_ctas_per_sm(steps, P.n_spans == 1, P.n_r, P.mixed != 0, P.slow_tiny != 0);
   if (per_sm <= 0) return fail(UWB_CUDA_ERROR, "integrand kernel cannot be resident");
   pr->grid_ctas = c->sm_count * per_sm;
+  // Split evaluation: the rows' point setup runs beside the Raman ODE (which
+  // holds one SM for ~2 ms) and the integrand proper only walks the listed
+  // points.  One record slot per (row, column); falls back to the fused
+  // kernel when the lists do not fit the budget (UWB_NLI_SPLIT_MB, default 8 GB).
+  P.plist = nullptr;
+  P.plist_n = nullptr;
+  pr->setup_ctas = 0;
+  if (nli_split_ok(P) && P.total_rows > 0) {
+    static const double budget_mb = [] {
+      const char* e = std::getenv("UWB_NLI_SPLIT_MB");
+      return e ? std::atof(e) : 8192.0;
+    }();
+    const size_t bytes = static_cast<size_t>(P.total_rows) * P.n_r * nli_point_record_bytes();
+    const int sp = nli_setup_ctas_per_sm();
+    if (sp > 0 && static_cast<double>(bytes) <= budget_mb * 1048576.0) {
+      P.plist = c->plist.get<unsigned char>(bytes);
+      P.plist_n = c->plist_n.get<int>(P.total_rows);
+      if (!P.plist || !P.plist_n) {
+        cudaGetLastError();  // a failed allocation: the fused kernel instead
+        P.plist = nullptr;
+        P.plist_n = nullptr;
+      } else {
+        pr->setup_ctas = std::max(1, c->sm_count - 1) * sp;  // leave the ODE's SM alone
+      }
+    }
+  }
   if (!P.log2rho || !P.zedge || !P.zstart || !P.zmid || !P.width || !P.wlast || !P.probe_nu ||
       !P.probe_chan || !P.hl2 || !P.rowsum || !P.rowpar || !P.counter || !P.n_eval || !P.probe_work || !P.rowcnt ||
       !F.probe_gamma ||
@@ -489,11 +515,31 @@ int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_sta
   // (a batch keeps the first failure: atomicExch writes are never cleared)
   if (reset_status) cudaMemsetAsync(pr->d_status, 0, sizeof(int), st);
   cudaEventRecord(c->ev0, st);
+  const bool split = pr->P.plist && pr->P.n_probes > 0;
+  if (split) {
+    if (!c->s_setup) {
+      cudaError_t e = cudaStreamCreateWithFlags(&c->s_setup, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(e, "split evaluation stream");
+    }
+    cudaEventRecord(c->ev_fork, st);  // the PSD copy and status reset above come first
+  }
   const int lo = launch_raman_ode(pr->O, pr->P.freq, pr->d_psd, pr->P.bch, pr->d_aeff,
                                   pr->aeff_ref, st);
   if (lo < 0) return fail(UWB_CUDA_ERROR, "raman ODE launch failed");
   launches += lo;
-  if (pr->P.n_probes > 0) {
+  if (split) {
+    cudaStreamWaitEvent(c->s_setup, c->ev_fork, 0);
+    const int ls = launch_nli_setup(pr->P, pr->setup_ctas, c->s_setup);
+    if (ls < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
+    cudaEventRecord(c->ev_join, c->s_setup);
+    cudaStreamWaitEvent(st, c->ev_join, 0);
+    const int ln = launch_nli_lists(pr->P, pr->F, pr->grid_ctas, st, c->evk0, c->evk1);
+    if (ln < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
+    launches += ls + ln;
+    c->nli_events_valid = true;
+  } else if (pr->P.n_probes > 0) {
     const int ln = launch_nli(pr->P, pr->F, pr->grid_ctas, st, c->evk0, c->evk1);
     if (ln < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
     launches += ln;

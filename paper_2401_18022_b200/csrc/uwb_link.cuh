@@ -54,6 +54,7 @@ struct uwb_ctx::Prepared {
   long long* d_rhs = nullptr;
   double* d_psd = nullptr;  // the NLI/ODE/link read launch PSD from here
   int grid_ctas = 0;
+  int setup_ctas = 0;  // split evaluation (P.plist set): the setup pass's grid
   int launches = 0;
 };
 

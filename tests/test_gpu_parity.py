@@ -284,6 +284,48 @@ print(json.dumps({"q": np.asarray(r.quadrant).ravel().tolist(), "eta": np.asarra
     assert _rel(on["eta"], off["eta"]) < 1e-13
 
 
+def test_split_evaluation_bit_identical_to_fused():
+    """evaluate_link's split integrand (nli_setup_kernel beside the Raman ODE,
+    then nli_list_kernel over the listed points) keeps the fused kernel's
+    point order and group sums, so the report is bit-identical to the fused
+    nli_rows_kernel's (UWB_NLI_NO_SPLIT=1), on a profile with dark channels
+    and an odd n_r (a self-mirrored middle column)."""
+    import json
+    import subprocess
+    import sys
+
+    code = r'''
+import json
+import numpy as np
+import paper_2401_18022_b200 as uwb
+eng = uwb.Engine(0)
+grid = uwb.make_default_uwb_grid()
+uwb.set_uniform_launch(grid, 1e-3)
+rng = np.random.default_rng(3)
+psd = np.array(grid.psd) * (1.0 + 0.3 * rng.random(grid.size()))
+psd[rng.random(grid.size()) < 0.05] = 0.0
+grid.psd = psd
+out = {}
+for n_r, dens in ((41, 0.95), (150, 1.4)):
+    lc = uwb.LinkConfig(gn=uwb.GnSolverConfig(n_r=n_r, mean_step_density=dens))
+    r = uwb.evaluate_link(uwb.default_fibre(), grid, lc, engine=eng)
+    st = eng.last_nli_stats()
+    out[str(n_r)] = {"eta": [float(x).hex() for x in np.asarray(r.eta)],
+                     "loss": float(r.loss_value).hex(), "evaluated": st["evaluated_points"],
+                     "active": st["active_points"]}
+print(json.dumps(out))
+'''
+    out = {}
+    for flag in ("0", "1"):
+        env = dict(os.environ, UWB_NLI_NO_SPLIT=flag)
+        p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           timeout=600, cwd=ROOT)
+        assert p.returncode == 0, p.stderr
+        out[flag] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert out["0"] == out["1"]
+    assert out["0"]["41"]["active"] > 0
+
+
 @pytest.mark.parametrize("kw", [
     dict(n_r=41),                                   # odd n_r: the middle column is its own mirror
     dict(n_r=33, u1_uniform=1),                     # uniform u1 edges
