@@ -486,7 +486,13 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
         P.plist = nullptr;
         P.plist_n = nullptr;
       } else {
-        pr->setup_ctas = std::max(1, c->sm_count - 1) * sp;  // leave the ODE's SM alone
+        static const int setup_env = [] {  // UWB_NLI_SETUP_CTAS: the setup pass's grid (A/B)
+          const char* e = std::getenv("UWB_NLI_SETUP_CTAS");
+          return e ? std::atoi(e) : 0;
+        }();
+        // two CTAs per SM, the ODE's SM left alone: the third resident CTA per
+        // SM slowed the concurrent ODE by 4 % (profiles/r02_integrand_experiments.md)
+        pr->setup_ctas = setup_env > 0 ? setup_env : std::max(1, c->sm_count - 1) * std::min(sp, 2);
       }
     }
   }

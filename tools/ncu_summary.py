@@ -1,6 +1,6 @@
 """Summarise an ncu report: key throughput metrics, stall reasons, SASS mix.
 
-    python tools/ncu_summary.py gpurun_out/prof.ncu-rep [steps_per_launch]
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep [steps_per_launch] [kernel-regex]
 """
 import csv
 import io
@@ -10,11 +10,13 @@ import sys
 from collections import Counter
 
 rep = sys.argv[1]
-steps = float(sys.argv[2]) if len(sys.argv) > 2 else None
+steps = float(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] != "-" else None
+kfilt = ["--kernel-name", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
 
 
 def page(*args):
-    out = subprocess.run(["ncu", "-i", rep, *args, "--csv"], capture_output=True, text=True).stdout
+    out = subprocess.run(["ncu", "-i", rep, *kfilt, *args, "--csv"], capture_output=True,
+                         text=True).stdout
     return list(csv.reader(io.StringIO(out)))
 
 
@@ -42,8 +44,15 @@ print("-- stall reasons (top)")
 for k, val in sorted(stalls.items(), key=lambda kv: -kv[1])[:10]:
     print(f"   {k:90s} {val:8.2f}")
 src = page("--page", "source", "--print-source", "sass")
-hh = src[1]
-rows = [dict(zip(hh, r)) for r in src[2:] if len(r) == len(hh)]
+# one section per profiled kernel: a name row, then a header row starting "Address"
+hi = next(i for i, r in enumerate(src) if r and r[0] == "Address")
+hh = src[hi]
+rows = []
+for r in src[hi + 1:]:
+    if r and r[0] == "Address":
+        break  # the next kernel's section
+    if len(r) == len(hh):
+        rows.append(dict(zip(hh, r)))
 tot = sum(int(r["Instructions Executed"]) for r in rows)
 c = Counter()
 for r in rows:
