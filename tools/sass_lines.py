@@ -29,7 +29,12 @@ for l in txt[start + 1:]:
         idx2.append(cur)
 rows = list(csv.reader(open(sass_csv)))
 h = rows[1]
-data = [dict(zip(h, r)) for r in rows[2:] if len(r) == len(h)]
+data = []
+for r in rows[2:]:
+    if r and r[0] in ("Kernel Name", "Address"):
+        break  # the next kernel's section
+    if len(r) == len(h):
+        data.append(dict(zip(h, r)))
 agg = defaultdict(float)
 stall = defaultdict(float)
 for i, d in enumerate(data):
