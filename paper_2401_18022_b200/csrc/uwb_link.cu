@@ -466,11 +466,13 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   pr->grid_ctas = c->sm_count * per_sm;
   // Split evaluation: the rows' point setup runs beside the Raman ODE (which
   // holds one SM for ~2 ms) and the integrand proper only walks the listed
-  // points.  One record slot per (row, column); falls back to the fused
-  // kernel when the lists do not fit the budget (UWB_NLI_SPLIT_MB, default 8 GB).
+  // points.  One record slot per (row, column), allocated by
+  // the first single evaluation (batches keep the fused kernel); the fused
+  // kernel when the lists exceed the budget (UWB_NLI_SPLIT_MB, default 8 GB).
   P.plist = nullptr;
   P.plist_n = nullptr;
   pr->setup_ctas = 0;
+  pr->split_bytes = 0;
   if (nli_split_ok(P) && P.total_rows > 0) {
     static const double budget_mb = [] {
       const char* e = std::getenv("UWB_NLI_SPLIT_MB");
@@ -479,21 +481,14 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
     const size_t bytes = static_cast<size_t>(P.total_rows) * P.n_r * nli_point_record_bytes();
     const int sp = nli_setup_ctas_per_sm();
     if (sp > 0 && static_cast<double>(bytes) <= budget_mb * 1048576.0) {
-      P.plist = c->plist.get<unsigned char>(bytes);
-      P.plist_n = c->plist_n.get<int>(P.total_rows);
-      if (!P.plist || !P.plist_n) {
-        cudaGetLastError();  // a failed allocation: the fused kernel instead
-        P.plist = nullptr;
-        P.plist_n = nullptr;
-      } else {
-        static const int setup_env = [] {  // UWB_NLI_SETUP_CTAS: the setup pass's grid (A/B)
-          const char* e = std::getenv("UWB_NLI_SETUP_CTAS");
-          return e ? std::atoi(e) : 0;
-        }();
-        // two CTAs per SM, the ODE's SM left alone: the third resident CTA per
-        // SM slowed the concurrent ODE by 4 % (profiles/r02_integrand_experiments.md)
-        pr->setup_ctas = setup_env > 0 ? setup_env : std::max(1, c->sm_count - 1) * std::min(sp, 2);
-      }
+      static const int setup_env = [] {  // UWB_NLI_SETUP_CTAS: the setup pass's grid (A/B)
+        const char* e = std::getenv("UWB_NLI_SETUP_CTAS");
+        return e ? std::atoi(e) : 0;
+      }();
+      // two CTAs per SM, the ODE's SM left alone: the third resident CTA per
+      // SM slowed the concurrent ODE by 4 % (profiles/r02_integrand_experiments.md)
+      pr->setup_ctas = setup_env > 0 ? setup_env : std::max(1, c->sm_count - 1) * std::min(sp, 2);
+      pr->split_bytes = bytes;
     }
   }
   if (!P.log2rho || !P.zedge || !P.zstart || !P.zmid || !P.width || !P.wlast || !P.probe_nu ||
@@ -521,6 +516,16 @@ int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_sta
   // (a batch keeps the first failure: atomicExch writes are never cleared)
   if (reset_status) cudaMemsetAsync(pr->d_status, 0, sizeof(int), st);
   cudaEventRecord(c->ev0, st);
+  if (pr->split_bytes && !pr->P.plist && pr->P.n_probes > 0) {
+    pr->P.plist = c->plist.get<unsigned char>(pr->split_bytes);
+    pr->P.plist_n = c->plist_n.get<int>(pr->P.total_rows);
+    if (!pr->P.plist || !pr->P.plist_n) {  // out of memory: the fused kernel from now on
+      cudaGetLastError();
+      pr->P.plist = nullptr;
+      pr->P.plist_n = nullptr;
+      pr->split_bytes = 0;
+    }
+  }
   const bool split = pr->P.plist && pr->P.n_probes > 0;
   if (split) {
     if (!c->s_setup) {

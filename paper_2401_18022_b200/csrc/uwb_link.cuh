@@ -54,7 +54,8 @@ struct uwb_ctx::Prepared {
   long long* d_rhs = nullptr;
   double* d_psd = nullptr;  // the NLI/ODE/link read launch PSD from here
   int grid_ctas = 0;
-  int setup_ctas = 0;  // split evaluation (P.plist set): the setup pass's grid
+  int setup_ctas = 0;      // split evaluation: the setup pass's grid (0: fused kernel)
+  size_t split_bytes = 0;  // its point lists, allocated by the first single evaluation
   int launches = 0;
 };
 
