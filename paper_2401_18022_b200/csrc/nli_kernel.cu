@@ -257,7 +257,32 @@ __device__ __forceinline__ void init_step_tabs(const StepTabs& T, int i) {
 
 // 2^(x/16) (uwb_devmath.cuh step_exp2_16; the same value bit for bit: the
 // power-of-two scale is applied to the table entry before the product)
+#ifndef UWB_EXP2_NOTAB
+#define UWB_EXP2_NOTAB 0
+#endif
+#if UWB_EXP2_NOTAB
+// table-free variant (A/B): 2^(x/16) = 2^n 2^f, f in [-1/2, 1/2], degree-8
+// fit (relative error 1.1e-12), 2^n inserted into the exponent field
+__constant__ double c_e8[9] = {1.0, 0.6931471805465779, 0.24022650699046685,
+                               0.055504109391347665, 0.009618128509058098,
+                               0.0013333452228655083, 0.00015403873617090126,
+                               1.5309699242759908e-05, 1.3171450610841097e-06};
+#endif
 __device__ __forceinline__ double step_exp2_16t(double x, const StepTabs& T) {
+#if UWB_EXP2_NOTAB
+  const double t = fma(x, 0.0625, kMagic);
+  const int n = __double2loint(t);
+  const double f = fma(x, 0.0625, -(t - kMagic));
+  double q = fma(f, c_e8[8], c_e8[7]);
+  q = fma(q, f, c_e8[6]);
+  q = fma(q, f, c_e8[5]);
+  q = fma(q, f, c_e8[4]);
+  q = fma(q, f, c_e8[3]);
+  q = fma(q, f, c_e8[2]);
+  q = fma(q, f, c_e8[1]);
+  q = fma(q, f, 1.0);
+  return __hiloint2double(__double2hiint(q) + (n << 20), __double2loint(q));
+#else
   const double t = x + kMagic;
   const int k = __double2loint(t);
   const double r = x - (t - kMagic);
@@ -267,6 +292,7 @@ __device__ __forceinline__ double step_exp2_16t(double x, const StepTabs& T) {
   p = fma(p, r, 1.0);
   const double v = T.e2c[k & 15];
   return __hiloint2double(__double2hiint(v) + (k << 16), __double2loint(v)) * p;
+#endif
 }
 
 
@@ -322,8 +348,44 @@ __constant__ double c_c8[4] = {kStep8C0, kStep8C1, kStep8C2, kInvPio8};
 
 constexpr double kUnitInv = kInvPio8;  // 1 / (the phase unit pi/8)
 
+#ifndef UWB_SINCOS_NOTAB
+#define UWB_SINCOS_NOTAB 1
+#endif
+#if UWB_SINCOS_NOTAB
+// Shipping phasor (uwb_devmath.cuh step_sincos8q, same operation sequence):
+// reduction to multiples of pi/2 (k = rint(phi8 z / 4) by a 1.5 * 2^54
+// shifter, r = phi8 z - 4k in [-2, 2] pi/8 units), sin degree 9 (2.5e-12) and
+// cos degree 10 (1.4e-13) with the powers of pi/8 folded in, then the
+// quarter-turn rotation by a swap and two sign flips of the high word: 14 FP64
+// instructions and no table (the pi/8 version: 15 FP64 and a bank-conflicted
+// LDS.128, 5.5 of the ~26 LSU wavefronts per warp-step; 7.62 -> 7.12 ms).
+__constant__ double c_s8q[4] = {kStepQS0, kStepQS1, kStepQS2, kStepQS3};
+__constant__ double c_c8q[5] = {kStepQC0, kStepQC1, kStepQC2, kStepQC3, kStepQC4};
+#endif
 __device__ __forceinline__ void step_sincos8(double phi8, double z, const StepTabs& T,
                                              double* c_out, double* s_out) {
+#if UWB_SINCOS_NOTAB
+  constexpr double kMagic4 = 4.0 * kMagic;
+  const double t4 = fma(phi8, z, kMagic4);
+  const int q4 = __double2loint(t4);
+  const double kd4 = t4 - kMagic4;
+  const double r4 = fma(phi8, z, -kd4);
+  const double z4 = r4 * r4;
+  double ps4 = fma(z4, c_s8q[3], c_s8q[2]);
+  ps4 = fma(ps4, z4, c_s8q[1]);
+  ps4 = fma(ps4, z4, c_s8q[0]);
+  const double sr4 = fma(r4 * z4, ps4, r4);
+  double pc4 = fma(z4, c_c8q[4], c_c8q[3]);
+  pc4 = fma(pc4, z4, c_c8q[2]);
+  pc4 = fma(pc4, z4, c_c8q[1]);
+  pc4 = fma(pc4, z4, c_c8q[0]);
+  const double cr4 = fma(pc4, z4, kInvPio8);
+  const bool sw = (q4 & 1) != 0;
+  const double c4 = sw ? sr4 : cr4, s4 = sw ? cr4 : sr4;
+  *c_out = __hiloint2double(__double2hiint(c4) ^ (((q4 + 1) & 2) << 30), __double2loint(c4));
+  *s_out = __hiloint2double(__double2hiint(s4) ^ ((q4 & 2) << 30), __double2loint(s4));
+  return;
+#endif
   const double t = fma(phi8, z, kMagic);
   const int q = __double2loint(t) & 15;
   const double kd = t - kMagic;

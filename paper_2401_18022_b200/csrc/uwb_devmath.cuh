@@ -341,7 +341,51 @@ constexpr double kStep8C1 = 0.0025232960009761362;
 constexpr double kStep8C2 = -1.2957417140207165e-05;
 constexpr double kInvPio8 = 2.5464790894703255;  // RN(8/pi) = 1/a
 
-// nli_kernel.cu step_sincos8 (same operation sequence): (cos, sin)(phi z) / a.
+// Quarter-turn variant without the (cos, sin)(q pi/8) table (the shipping
+// nli_kernel.cu step_sincos8, UWB_SINCOS_NOTAB=1): k = rint(phi8 z / 4) by a
+// 1.5 * 2^54 shifter (its ulp is 4), r = phi8 z - 4k in [-2, 2] by one FMA
+// (|a r| <= pi/4), then
+//   sin(a r)/a = r + r^3 (QS0 + r^2 (QS1 + r^2 (QS2 + r^2 QS3)))     (2.5e-12 abs)
+//   cos(a r)/a = 1/a + r^2 (QC0 + r^2 (QC1 + ... + r^2 QC4))           (1.4e-13 abs)
+// and the rotation by k pi/2 as a swap (k odd) and two sign flips.  Fits:
+// weighted least squares on 6000 Chebyshev nodes of r^2 in [0, 4], refined in
+// long double (errors measured against long-double libm; tests/test_devmath.py).
+// The rotation has no arithmetic, so the phasor costs 14 FP64 instructions (the
+// table version 15) and no shared-memory lookup.
+constexpr double kStepQS0 = -0.025702094732684134;
+constexpr double kStepQS1 = 0.00019817917932534872;
+constexpr double kStepQS2 = -7.275778874298369e-07;
+constexpr double kStepQS3 = 1.53596213791826e-09;
+constexpr double kStepQC0 = -0.19634954084614456;
+constexpr double kStepQC1 = 0.0025232972466868123;
+constexpr double kStepQC2 = -1.2970795849995253e-05;
+constexpr double kStepQC3 = 3.571476152561739e-08;
+constexpr double kStepQC4 = -6.0315590453199e-11;
+
+UWB_HD void step_sincos8q(double phi8, double z, double* c_out, double* s_out) {
+  constexpr double kMagic4 = 4.0 * kMagic;
+  const double t = fmad(phi8, z, kMagic4);
+  const int q = lo_word(t);
+  const double kd = t - kMagic4;
+  const double r = fmad(phi8, z, -kd);
+  const double zz = r * r;
+  double ps = fmad(zz, kStepQS3, kStepQS2);
+  ps = fmad(ps, zz, kStepQS1);
+  ps = fmad(ps, zz, kStepQS0);
+  const double sr = fmad(r * zz, ps, r);
+  double pc = fmad(zz, kStepQC4, kStepQC3);
+  pc = fmad(pc, zz, kStepQC2);
+  pc = fmad(pc, zz, kStepQC1);
+  pc = fmad(pc, zz, kStepQC0);
+  const double cr = fmad(pc, zz, kInvPio8);
+  const bool sw = (q & 1) != 0;
+  const double c = sw ? sr : cr, s = sw ? cr : sr;
+  *c_out = ((q + 1) & 2) ? -c : c;
+  *s_out = (q & 2) ? -s : s;
+}
+
+// nli_kernel.cu step_sincos8 with UWB_SINCOS_NOTAB=0 (same operation
+// sequence): (cos, sin)(phi z) / a.
 UWB_HD void step_sincos8(double phi8, double z, const double* cos16, const double* sin16,
                          double* c_out, double* s_out) {
   const double t = fmad(phi8, z, kMagic);

@@ -51,6 +51,14 @@ double err_step_sincos8(const double* phi8, const double* z, long n, int which) 
   long double x = a * ((long double)fmod(k, 16.0) + r);
   long double ec = fabsl(c * a - cosl(x)), es = fabsl(s * a - sinl(x));
   long double e = which == 0 ? ec : es; if (e > m) m = e; } return (double)m; }
+double err_step_sincos8q(const double* phi8, const double* z, long n, int which) { long double m = 0;
+  const long double a = 3.14159265358979323846264338327950288L / 8; for (long i = 0; i < n; ++i) {
+  double c, s; uwb::step_sincos8q(phi8[i], z[i], &c, &s);
+  const double k = rint(phi8[i] * z[i]);
+  const long double r = fmal((long double)phi8[i], (long double)z[i], -(long double)k);
+  long double x = a * ((long double)fmod(k, 16.0) + r);
+  long double ec = fabsl(c * a - cosl(x)), es = fabsl(s * a - sinl(x));
+  long double e = which == 0 ? ec : es; if (e > m) m = e; } return (double)m; }
 double err_sincos(const double* x, long n) { long double m = 0; for (long i = 0; i < n; ++i) {
   double c, s; uwb::sincos_rd(x[i], &c, &s); long double ec = fabsl(c - cosl((long double)x[i])), es = fabsl(s - sinl((long double)x[i]));
   if (ec > m) m = ec; if (es > m) m = es; } return (double)m; }
@@ -74,6 +82,7 @@ def lib(tmp_path_factory):
     L.err_step_exp2_16.restype = ctypes.c_double
     L.err_step_sincos16.restype = ctypes.c_double
     L.err_step_sincos8.restype = ctypes.c_double
+    L.err_step_sincos8q.restype = ctypes.c_double
     return L
 
 
@@ -152,6 +161,35 @@ def test_step_sincos8_error_bounds(lib, scale):
     ec = lib.err_step_sincos8(_p(phi8), _p(z), len(z), 0)
     es = lib.err_step_sincos8(_p(phi8), _p(z), len(z), 1)
     assert 1e-13 < ec < 1.75e-12 and 1e-13 < es < 1.75e-12, (ec, es)
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e3, 1e5, 3e7])
+def test_step_sincos8q_error_bounds(lib, scale):
+    """The shipping fast-branch phasor (step_sincos8q = nli_kernel.cu
+    step_sincos8 at UWB_SINCOS_NOTAB=1): quarter-turn reduction, sin degree 9,
+    cos degree 10, swap + sign flips.  cos and sin each within 2.75e-12
+    absolute of long double (the sin fit's 2.5e-12 lands in either after the
+    swap), and a real truncation (> 1e-13)."""
+    rng = np.random.default_rng(7)
+    z = rng.uniform(0.0, 2e5, 300000)
+    phi8 = rng.uniform(-1.0, 1.0, len(z)) * scale / 2e5 * 8 / np.pi
+    ec = lib.err_step_sincos8q(_p(phi8), _p(z), len(z), 0)
+    es = lib.err_step_sincos8q(_p(phi8), _p(z), len(z), 1)
+    assert 1e-13 < max(ec, es) and ec < 2.75e-12 and es < 2.75e-12, (ec, es)
+
+
+def test_step_sincos8q_quadrants_and_device_coefficients(lib):
+    """Every quarter turn (k mod 4 = 0..3, negative k included) lands on the
+    right (cos, sin); the device constant banks are the header's kStepQ*."""
+    phi8 = np.array([0.0, 1.0, 2.0, 3.0, 4.0, 5.0, 6.0, 7.0, 8.0, 12.0, -4.0, -8.0, -12.0, 9.9])
+    z = np.ones_like(phi8)
+    ec = lib.err_step_sincos8q(_p(phi8), _p(z), len(z), 0)
+    es = lib.err_step_sincos8q(_p(phi8), _p(z), len(z), 1)
+    assert ec < 2.75e-12 and es < 2.75e-12, (ec, es)
+    dev = open(os.path.join(ROOT, "paper_2401_18022_b200", "csrc", "nli_kernel.cu")).read()
+    assert "c_s8q[4] = {kStepQS0, kStepQS1, kStepQS2, kStepQS3}" in dev
+    assert "c_c8q[5] = {kStepQC0, kStepQC1, kStepQC2, kStepQC3, kStepQC4}" in dev
+    assert "#define UWB_SINCOS_NOTAB 1" in dev
 
 
 def test_step_sincos8_coefficients_are_the_scaled_fits():
