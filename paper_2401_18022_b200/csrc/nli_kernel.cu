@@ -230,6 +230,20 @@ struct StepTabs {
   double* z;      // [128] the span's end-edge positions (HOIST, K <= 8), lane order
 };
 
+// nli_list_kernel's per-warp records: a chunk of kListChunk listed points
+// plus up to 3 carried over, and the probe half-log column (no per-lane |K|^2
+// or row fields: the fused kernel's WarpSmem is ~40 % larger, and what the
+// list kernel does not hold in shared memory the carveout leaves to L1)
+#ifndef UWB_LIST_CHUNK
+#define UWB_LIST_CHUNK 16
+#endif
+constexpr int kListChunk = UWB_LIST_CHUNK;
+struct ListWarpSmem {
+  PointRec pt[kListChunk + 4];
+  alignas(16) double h[128];
+};
+__device__ __forceinline__ double* S_h(ListWarpSmem& S) { return S.h; }
+
 __device__ __forceinline__ double* S_h(WarpSmem& S) {
 #if UWB_SEG8
   return S.h;
@@ -639,8 +653,8 @@ __device__ __forceinline__ double point_kernel(const NliParams& P, const WarpSme
 // and the 3-level reduction tree are amortised over 2K steps instead of K.
 // The probe half-logs come from a per-warp shared column (S.h), the z edges
 // from the CTA-wide one, both as 16-byte pairs.
-template <int K, bool FULL, bool TINY>
-__device__ __forceinline__ double point_kernel8(const NliParams& P, const WarpSmem& S, int idx,
+template <int K, bool FULL, bool TINY, class WS>
+__device__ __forceinline__ double point_kernel8(const NliParams& P, const WS& S, int idx,
                                                 int s8, bool z0zero, const StepTabs& TB) {
   constexpr int NS = 16 * K;
   const PointRec& R = S.pt[idx];
@@ -658,7 +672,7 @@ __device__ __forceinline__ double point_kernel8(const NliParams& P, const WarpSm
   const double2* ca = reinterpret_cast<const double2*>(P.log2rho + cl.x + l2);
   const double2* cb = reinterpret_cast<const double2*>(P.log2rho + cl.y + l2);
   const double2* cc3 = reinterpret_cast<const double2*>(P.log2rho + cl.z + l2);
-  const double2* hs = reinterpret_cast<const double2*>(S_h(const_cast<WarpSmem&>(S)) + l2);
+  const double2* hs = reinterpret_cast<const double2*>(S_h(const_cast<WS&>(S)) + l2);
   const double2* zs = reinterpret_cast<const double2*>(TB.z + l2);
   constexpr int NS2 = NS / 2;  // the column stride in double2 units
   const int N = P.steps;
@@ -1298,7 +1312,7 @@ __global__ void __launch_bounds__(UWB_NLI_WARPS * 32, UWB_NLI_MIN_BLOCKS)
     nli_list_kernel(const NliParams P) {
   constexpr int kWarps = UWB_NLI_WARPS;
   constexpr int NS = 16 * K;
-  __shared__ WarpSmem s_w[kWarps];
+  __shared__ ListWarpSmem s_w[kWarps];
   __shared__ double2 s_tab_cs16[16];
   __shared__ double s_tab_e2c[16];
   __shared__ __align__(16) double s_tab_z[128];
@@ -1309,7 +1323,7 @@ __global__ void __launch_bounds__(UWB_NLI_WARPS * 32, UWB_NLI_MIN_BLOCKS)
   if (threadIdx.x < NS) s_tab_z[threadIdx.x] = __ldg(P.zedge + threadIdx.x);
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  WarpSmem& S = s_w[threadIdx.x >> 5];
+  ListWarpSmem& S = s_w[threadIdx.x >> 5];
   const int n_r = P.n_r;
   const int per_probe = P.n_q * n_r;
   const bool z0zero = __ldg(P.zstart) == 0.0;
@@ -1334,8 +1348,8 @@ __global__ void __launch_bounds__(UWB_NLI_WARPS * 32, UWB_NLI_MIN_BLOCKS)
     int n_pend = 0;
     double row_acc = 0.0;
     const int sg = lane >> 3, s8 = lane & 7;
-    for (int c0 = 0; c0 < n; c0 += 32) {
-      const int cnt = min(32, n - c0);
+    for (int c0 = 0; c0 < n; c0 += kListChunk) {
+      const int cnt = min(kListChunk, n - c0);
       double2* dst = reinterpret_cast<double2*>(S.pt + n_pend);
       for (int t = lane; t < cnt * kRec2; t += 32) dst[t] = __ldcs(src + c0 * kRec2 + t);
       __syncwarp();
