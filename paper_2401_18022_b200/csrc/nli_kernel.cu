@@ -1307,10 +1307,19 @@ __global__ void __launch_bounds__(kSetupWarps * 32) nli_setup_kernel(const NliPa
   }
 }
 
+#ifndef UWB_LIST_WARPS
+// 10 warps x 2 CTAs (96 registers): the list kernel keeps no row setup, so it
+// fits in fewer registers than the fused kernel's 128; 8 / 9 / 11 / 12 warps
+// measured 7.09 / 7.17 / 8.10 / 7.74 ms against 7.00 (profiles/r02_integrand_experiments.md)
+#define UWB_LIST_WARPS 10
+#endif
+#ifndef UWB_LIST_MIN_BLOCKS
+#define UWB_LIST_MIN_BLOCKS UWB_NLI_MIN_BLOCKS
+#endif
 template <int K, bool FULL, bool TINY>
-__global__ void __launch_bounds__(UWB_NLI_WARPS * 32, UWB_NLI_MIN_BLOCKS)
+__global__ void __launch_bounds__(UWB_LIST_WARPS * 32, UWB_LIST_MIN_BLOCKS)
     nli_list_kernel(const NliParams P) {
-  constexpr int kWarps = UWB_NLI_WARPS;
+  constexpr int kWarps = UWB_LIST_WARPS;
   constexpr int NS = 16 * K;
   __shared__ ListWarpSmem s_w[kWarps];
   __shared__ double2 s_tab_cs16[16];
@@ -1852,7 +1861,14 @@ int launch_nli_lists(const NliParams& p, const FinalizeParams& f, int grid_ctas,
   ++launches;
   if (ev_k0) cudaEventRecord(ev_k0, stream);
   allow_row_smem(k, p.n_r);  // the same carveout rule as the fused kernel
-  k<<<grid_ctas, UWB_NLI_WARPS * 32, 0, stream>>>(p);
+  if (UWB_LIST_WARPS != UWB_NLI_WARPS || UWB_LIST_MIN_BLOCKS != UWB_NLI_MIN_BLOCKS) {
+    int dev = 0, sms = 0, per_sm = 0;  // a differently shaped list kernel (A/B builds)
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, UWB_LIST_WARPS * 32, 0);
+    grid_ctas = std::max(1, sms * per_sm);
+  }
+  k<<<grid_ctas, UWB_LIST_WARPS * 32, 0, stream>>>(p);
   ++launches;
   if (ev_k1) cudaEventRecord(ev_k1, stream);
   const size_t fin_smem = static_cast<size_t>(p.n_q) * p.n_r * sizeof(double);
