@@ -44,7 +44,7 @@ UNIT = "s"
 FLOPS_PER_STEP = 87.0  # SURVEY §8(d) frozen convention, FP64 flops per inner phasor step
 # FP64 flops the integrand actually EXECUTES per computed step, from the SASS
 # of its ncu capture (2 DFMA + DADD + DMUL, predicated-on thread instructions
-# over the inner steps; profiles/r02_quarter_nli_ncu_summary.txt): the convention
+# over the inner steps; profiles/r02_v8_nli_ncu_summary.txt): the convention
 # above counts the reference's arithmetic, this counts the device's.
 EXECUTED_FLOPS_PER_STEP = 56.31
 FP64_FLOPS_PER_SM_CLK = 128.0  # B200: 64 FP64 FMA per SM per clock
