@@ -242,7 +242,14 @@ int uwb_evaluate_link(uwb_ctx* ctx, const uwb_grid* grid, const uwb_fibre* fibre
  *
  * The skip set is re-derived from each call's launch profile, like the
  * reference (guard or psd <= 0, gn_integral.hpp:349-352): a channel that was
- * dark at prepare time and is lit in a later call gets its NLI. */
+ * dark at prepare time and is lit in a later call gets its NLI.
+ *
+ * Memory: single evaluations (uwb_evaluate_link, _resident) run the rows'
+ * point setup beside the Raman ODE and keep one 96-byte record slot per
+ * (row, column) in HBM, allocated by the first such call on a prepared link:
+ * 4 * n_r^2 * 96 bytes per probe (5.1 GB for 589 channels at N_R = 150).
+ * Lists over UWB_NLI_SPLIT_MB (default 8192) or a failed allocation fall back
+ * to the fused integrand kernel (same results, bit for bit). */
 int uwb_evaluate_link_prepare(uwb_ctx* ctx, const uwb_grid* grid, const uwb_fibre* fibre,
                               const uwb_link_cfg* link, const uwb_nli_cfg* cfg);
 int uwb_evaluate_link_resident(uwb_ctx* ctx, const double* psd_dev, double* report_dev,
