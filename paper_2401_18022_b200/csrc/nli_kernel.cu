@@ -1834,6 +1834,16 @@ bool nli_split_ok(const NliParams& p) {
 
 size_t nli_point_record_bytes() { return sizeof(PointRec); }
 
+int nli_list_ctas_per_sm(const NliParams& p) {
+  ListKernel k = list_kernel_for(p);
+  if (!k) return 0;
+  allow_row_smem(k, p.n_r);
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, UWB_LIST_WARPS * 32, 0) != cudaSuccess)
+    return 0;
+  return n;
+}
+
 int nli_setup_ctas_per_sm() {
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, nli_setup_kernel, kSetupWarps * 32, 0) !=
@@ -1861,13 +1871,6 @@ int launch_nli_lists(const NliParams& p, const FinalizeParams& f, int grid_ctas,
   ++launches;
   if (ev_k0) cudaEventRecord(ev_k0, stream);
   allow_row_smem(k, p.n_r);  // the same carveout rule as the fused kernel
-  if (UWB_LIST_WARPS != UWB_NLI_WARPS || UWB_LIST_MIN_BLOCKS != UWB_NLI_MIN_BLOCKS) {
-    int dev = 0, sms = 0, per_sm = 0;  // a differently shaped list kernel (A/B builds)
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, UWB_LIST_WARPS * 32, 0);
-    grid_ctas = std::max(1, sms * per_sm);
-  }
   k<<<grid_ctas, UWB_LIST_WARPS * 32, 0, stream>>>(p);
   ++launches;
   if (ev_k1) cudaEventRecord(ev_k1, stream);

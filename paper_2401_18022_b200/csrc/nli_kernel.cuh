@@ -142,6 +142,7 @@ int launch_nli(const NliParams& p, const FinalizeParams& f, int grid_ctas, cudaS
 // are bit-identical to launch_nli's.
 bool nli_split_ok(const NliParams& p);
 size_t nli_point_record_bytes();
+int nli_list_ctas_per_sm(const NliParams& p);  // resident nli_list_kernel CTAs per SM
 int nli_setup_ctas_per_sm();
 int launch_nli_setup(const NliParams& p, int grid_ctas, cudaStream_t side);
 int launch_nli_lists(const NliParams& p, const FinalizeParams& f, int grid_ctas,

@@ -472,6 +472,7 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
   P.plist = nullptr;
   P.plist_n = nullptr;
   pr->setup_ctas = 0;
+  pr->list_ctas = 0;
   pr->split_bytes = 0;
   if (nli_split_ok(P) && P.total_rows > 0) {
     static const double budget_mb = [] {
@@ -480,7 +481,9 @@ int prepare(uwb_ctx* c, const uwb_grid* g, const uwb_fibre* fb, const uwb_link_c
     }();
     const size_t bytes = static_cast<size_t>(P.total_rows) * P.n_r * nli_point_record_bytes();
     const int sp = nli_setup_ctas_per_sm();
-    if (sp > 0 && static_cast<double>(bytes) <= budget_mb * 1048576.0) {
+    const int lp = nli_list_ctas_per_sm(P);
+    if (sp > 0 && lp > 0 && static_cast<double>(bytes) <= budget_mb * 1048576.0) {
+      pr->list_ctas = c->sm_count * lp;
       static const int setup_env = [] {  // UWB_NLI_SETUP_CTAS: the setup pass's grid (A/B)
         const char* e = std::getenv("UWB_NLI_SETUP_CTAS");
         return e ? std::atoi(e) : 0;
@@ -546,7 +549,7 @@ int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_sta
     if (ls < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
     cudaEventRecord(c->ev_join, c->s_setup);
     cudaStreamWaitEvent(st, c->ev_join, 0);
-    const int ln = launch_nli_lists(pr->P, pr->F, pr->grid_ctas, st, c->evk0, c->evk1);
+    const int ln = launch_nli_lists(pr->P, pr->F, pr->list_ctas, st, c->evk0, c->evk1);
     if (ln < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
     launches += ls + ln;
     c->nli_events_valid = true;

@@ -55,6 +55,7 @@ struct uwb_ctx::Prepared {
   double* d_psd = nullptr;  // the NLI/ODE/link read launch PSD from here
   int grid_ctas = 0;
   int setup_ctas = 0;      // split evaluation: the setup pass's grid (0: fused kernel)
+  int list_ctas = 0;       // and the list pass's
   size_t split_bytes = 0;  // its point lists, allocated by the first single evaluation
   int launches = 0;
 };
