@@ -33,6 +33,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "nli_kernel.cuh"
 #include "uwb_devmath.cuh"
@@ -243,6 +244,14 @@ struct ListWarpSmem {
   alignas(16) double h[128];
 };
 __device__ __forceinline__ double* S_h(ListWarpSmem& S) { return S.h; }
+// the fused kernel's records on the point_kernel8 path (WarpSmem without kv)
+struct WarpSmemCarry {
+  PointRec pt[36];
+  alignas(16) double h[128];
+  double nu, f, s1, s2, su, u1, lo, du2;
+  int sym;
+};
+__device__ __forceinline__ double* S_h(WarpSmemCarry& S) { return S.h; }
 
 __device__ __forceinline__ double* S_h(WarpSmem& S) {
 #if UWB_SEG8
@@ -932,7 +941,9 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
                                   MIXED ? UWB_NLI_MIXED_MIN_BLOCKS : UWB_NLI_MIN_BLOCKS)
     nli_rows_kernel(const NliParams P) {
   constexpr int kWarps = WarpsFor<HOIST, MIXED>::value;
-  __shared__ WarpSmem s_w[kWarps];
+  // the point_kernel8 path keeps no per-lane |K|^2 (kv): its smaller records
+  using WS = typename std::conditional<UWB_SEG8 && HOIST && !MIXED, WarpSmemCarry, WarpSmem>::type;
+  __shared__ WS s_w[kWarps];
   __shared__ double2 s_tab_cs16[16];
   __shared__ double s_tab_e2c[16];
   __shared__ __align__(16) double s_tab_z[UWB_Z_SMEM ? 128 : 1];
@@ -957,7 +968,7 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
   const int warp = threadIdx.x >> 5;
   const int sl = lane & 15;
   const int seg = lane >> 4;
-  WarpSmem& S = s_w[warp];
+  WS& S = s_w[warp];
   const int per_probe = P.n_q * P.n_r;
   double Zr[K > 0 ? K : 1], Hr[K > 0 ? K : 1];
   int cur_probe = -1;
@@ -1164,18 +1175,18 @@ __global__ void __launch_bounds__(WarpsFor<HOIST, MIXED>::value * 32,
                                                     s_tabs, Zr, Hr);
           if (ok && sl == 0) S.kv[S.pt[idx].src] = kv;
         }
-      }
-      __syncwarp();
-      UWB_BOUND(!valid || (j >= 0 && j < n_r));
-      // row sum (gn_integral.hpp:288-305): each chunk's 32 column values by a
-      // fixed xor tree, chunks added in ascending order -- the order depends
-      // on (n_r, row symmetry) only, so rows are reproducible and independent of
-      // scheduling and partitioning, and no per-row array is kept
-      double v = (valid && active) ? pw * (need ? S.kv[lane] : S.kv[lane ^ 16]) : 0.0;
+        __syncwarp();
+        UWB_BOUND(!valid || (j >= 0 && j < n_r));
+        // row sum (gn_integral.hpp:288-305): each chunk's 32 column values by a
+        // fixed xor tree, chunks added in ascending order -- the order depends
+        // on (n_r, row symmetry) only, so rows are reproducible and independent of
+        // scheduling and partitioning, and no per-row array is kept
+        double v = (valid && active) ? pw * (need ? S.kv[lane] : S.kv[lane ^ 16]) : 0.0;
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-      row_acc += v;
-      __syncwarp();
+        for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+        row_acc += v;
+        __syncwarp();
+      }
     }
     if constexpr (kCarry) {
       if (n_pend > 0) {  // the row's last (at most three) points; idle segments repeat point 0
