@@ -227,6 +227,8 @@ int uwb_evaluate_link(uwb_ctx* ctx, const uwb_grid* grid, const uwb_fibre* fibre
  * uwb_evaluate_link_prepare once; each uwb_evaluate_link_resident call takes
  * launch powers already in device memory (psd_dev [n_ch], W/Hz) and leaves the
  * report in device memory.  stream: cudaStream_t or NULL for the context's.
+ * Calls on one context share its device buffers: issue them on one stream (or
+ * order them with events); the context joins its own side stream internally.
  *
  * Report layout (report_dev here, and each row of uwb_evaluate_link_many's
  * report_host), report_len = 4*n_ch + 3 + 2*n_bands doubles:
