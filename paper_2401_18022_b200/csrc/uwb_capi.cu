@@ -416,7 +416,7 @@ void uwb_ctx_destroy(uwb_ctx* c) {
     c->batch = nullptr;
   }
   if (c->s_setup) cudaStreamSynchronize(c->s_setup);
-  for (cudaEvent_t ev : {c->ev0, c->ev1, c->evk0, c->evk1, c->ev_fork, c->ev_join})
+  for (cudaEvent_t ev : {c->ev0, c->ev1, c->evk0, c->evk1, c->ev_fork, c->ev_join, c->ev_lists})
     if (ev) cudaEventDestroy(ev);
   if (c->s_setup) cudaStreamDestroy(c->s_setup);
   if (c->stream) cudaStreamDestroy(c->stream);

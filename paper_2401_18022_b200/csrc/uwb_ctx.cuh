@@ -79,6 +79,7 @@ struct uwb_ctx {
   uwb::DBuf plist, plist_n;
   cudaStream_t s_setup = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_lists = nullptr;  // the last list pass is done with the point lists
   // link evaluation state (raman ODE + assembly)
   uwb::DBuf alpha, aeff, raman_x, raman_y, nf_db, guard, rho_end, ode_work, ode_gwork, report, mid, edge;
   std::vector<int> subset;

@@ -535,6 +535,7 @@ int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_sta
       cudaError_t e = cudaStreamCreateWithFlags(&c->s_setup, cudaStreamNonBlocking);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_lists, cudaEventDisableTiming);
       if (e != cudaSuccess) return cuda_fail(e, "split evaluation stream");
     }
     cudaEventRecord(c->ev_fork, st);  // the PSD copy and status reset above come first
@@ -545,12 +546,16 @@ int run_noise(uwb_ctx* c, const double* psd_dev, cudaStream_t st, bool reset_sta
   launches += lo;
   if (split) {
     cudaStreamWaitEvent(c->s_setup, c->ev_fork, 0);
+    // the previous list pass may have run on another stream: it must be done
+    // reading the point lists before this setup pass rewrites them
+    cudaStreamWaitEvent(c->s_setup, c->ev_lists, 0);
     const int ls = launch_nli_setup(pr->P, pr->setup_ctas, c->s_setup);
     if (ls < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
     cudaEventRecord(c->ev_join, c->s_setup);
     cudaStreamWaitEvent(st, c->ev_join, 0);
     const int ln = launch_nli_lists(pr->P, pr->F, pr->list_ctas, st, c->evk0, c->evk1);
     if (ln < 0) return fail(UWB_CONFIG_ERROR, "unsupported step count");
+    cudaEventRecord(c->ev_lists, st);
     launches += ls + ln;
     c->nli_events_valid = true;
   } else if (pr->P.n_probes > 0) {
