@@ -407,8 +407,7 @@ __device__ __forceinline__ void step_sincos8(double phi8, double z, const StepTa
   const double c4 = sw ? sr4 : cr4, s4 = sw ? cr4 : sr4;
   *c_out = __hiloint2double(__double2hiint(c4) ^ (((q4 + 1) & 2) << 30), __double2loint(c4));
   *s_out = __hiloint2double(__double2hiint(s4) ^ ((q4 & 2) << 30), __double2loint(s4));
-  return;
-#endif
+#else
   const double t = fma(phi8, z, kMagic);
   const int q = __double2loint(t) & 15;
   const double kd = t - kMagic;
@@ -424,6 +423,7 @@ __device__ __forceinline__ void step_sincos8(double phi8, double z, const StepTa
   const double tc = cs.x, ts = cs.y;
   *c_out = fma(tc, cr, -(ts * sr));
   *s_out = fma(ts, cr, tc * sr);
+#endif
 }
 
 // ---- compensated-FP32 ("mixed") step arithmetic (GnSolverConfig precision
